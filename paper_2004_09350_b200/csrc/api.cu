@@ -1,0 +1,794 @@
+// api.cu — the C ABI of libms (include/ms.h): the paper's "column layer"
+// (P:469, 477-479): validates descriptors, splits columns into main part and
+// remainder (by descriptor), sizes and allocates outputs, launches the
+// kernels and performs the op's single read-back synchronisation.
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "launch.h"
+
+using namespace ms;
+
+__device__ uint32_t g_ms_sticky_err;  // errors of the non-synchronising ops
+
+namespace {
+
+constexpr uint64_t kAlign = 256;
+inline uint64_t align_up(uint64_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+inline bool is_block(int32_t f) { return f == MS_DYN_BP || f == MS_FOR_BP || f == MS_DELTA_BP; }
+inline bool valid_B(uint32_t B) { return B == 128 || B == 256 || B == 512 || B == 1024 || B == 2048; }
+inline uint32_t log2u(uint32_t x) { return 31u - (uint32_t)__builtin_clz(x); }
+inline uint32_t ebw_host(uint64_t x) { return x ? 64u - (uint32_t)__builtin_clzll(x) : 0u; }
+inline uint64_t words_for(uint64_t n, uint32_t w) { return (n * (uint64_t)w + 63) / 64; }
+
+struct Ctx {
+  const ms_ctx* c;
+  cudaStream_t s;
+  explicit Ctx(const ms_ctx* cc) : c(cc), s(cc ? (cudaStream_t)cc->stream : nullptr) {}
+  void* alloc(uint64_t bytes) const {
+    if (bytes == 0) bytes = kAlign;
+    if (c && c->alloc) return c->alloc(c->alloc_ctx, (size_t)bytes, c->stream);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  }
+  void free(void* p) const {
+    if (!p) return;
+    if (c && c->free) c->free(c->alloc_ctx, p, c->stream);
+    else cudaFreeAsync(p, s);
+  }
+};
+
+// One scratch allocation per op, carved into 256-byte aligned regions.
+struct Scratch {
+  const Ctx& ctx;
+  std::vector<uint64_t> zero_off, zero_len;
+  uint64_t size = 0;
+  char* base = nullptr;
+  explicit Scratch(const Ctx& c) : ctx(c) {}
+  ~Scratch() { ctx.free(base); }
+  uint64_t add(uint64_t bytes, bool zero) {
+    uint64_t off = size;
+    size = align_up(size + (bytes ? bytes : 8));
+    if (zero) {
+      zero_off.push_back(off);
+      zero_len.push_back(bytes ? bytes : 8);
+    }
+    return off;
+  }
+  bool commit() {
+    base = (char*)ctx.alloc(size ? size : kAlign);
+    if (!base) return false;
+    // coalesce the zero regions into one memset when they are dense enough
+    for (size_t i = 0; i < zero_off.size(); ++i)
+      if (cudaMemsetAsync(base + zero_off[i], 0, zero_len[i], ctx.s) != cudaSuccess) return false;
+    return true;
+  }
+  template <class T>
+  T* at(uint64_t off) const { return reinterpret_cast<T*>(base + off); }
+};
+
+ms_status status_from_bits(uint32_t bits) {
+  const ms_status order[] = {MS_E_CORRUPT, MS_E_RANGE, MS_E_WIDTH_OVERFLOW, MS_E_INVALID, MS_E_UNSUPPORTED,
+                             MS_E_NOMEM};
+  for (ms_status s : order)
+    if (bits & err_bit(s)) return s;
+  return MS_OK;
+}
+
+ms_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return MS_OK;
+  if (e == cudaErrorMemoryAllocation) return MS_E_NOMEM;
+  return MS_E_CUDA;
+}
+
+#define MS_TRY_CUDA(expr)                    \
+  do {                                       \
+    cudaError_t e_ = (expr);                 \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
+#define MS_TRY(expr)                         \
+  do {                                       \
+    ms_status s_ = (expr);                   \
+    if (s_ != MS_OK) return s_;              \
+  } while (0)
+
+ms_status check_fmt(const ms_fmt& f) {
+  switch (f.format) {
+    case MS_UNCOMPR:
+    case MS_RLE:
+      return MS_OK;
+    case MS_STATIC_BP:
+      return f.bit_width <= 64 ? MS_OK : MS_E_INVALID;
+    case MS_DYN_BP:
+    case MS_FOR_BP:
+    case MS_DELTA_BP:
+      return valid_B(f.block_size) ? MS_OK : MS_E_INVALID;
+    default:
+      return MS_E_UNSUPPORTED;
+  }
+}
+
+// descriptor consistency of an input column (host side)
+ms_status check_col(const ms_column* c) {
+  if (!c) return MS_E_INVALID;
+  const uint64_t n = c->n;
+  switch (c->fmt.format) {
+    case MS_UNCOMPR:
+      if (c->payload_words != n || (n && !c->payload)) return MS_E_INVALID;
+      return MS_OK;
+    case MS_STATIC_BP:
+      if (c->fmt.bit_width < 1 || c->fmt.bit_width > 64) return MS_E_INVALID;
+      if (c->payload_words != words_for(n, c->fmt.bit_width) || (n && !c->payload)) return MS_E_INVALID;
+      return MS_OK;
+    case MS_RLE:
+      if (c->payload_words != 2 * c->n_runs || (c->n_runs && !c->payload)) return MS_E_INVALID;
+      if ((c->n_runs == 0) != (n == 0) || c->n_runs > n) return MS_E_INVALID;
+      return MS_OK;
+    case MS_DYN_BP:
+    case MS_FOR_BP:
+    case MS_DELTA_BP: {
+      const uint32_t B = c->fmt.block_size;
+      if (!valid_B(B)) return MS_E_INVALID;
+      if (c->n_blocks != n / B || c->n_rem != n % B || !c->cw) return MS_E_INVALID;
+      if (c->fmt.format != MS_DYN_BP && c->n_blocks && !c->ref) return MS_E_INVALID;
+      if (c->n_rem && !c->rem) return MS_E_INVALID;
+      if (c->payload_words && !c->payload) return MS_E_INVALID;
+      if (c->payload_words % (B / 64)) return MS_E_CORRUPT;
+      return MS_OK;
+    }
+    default:
+      return MS_E_UNSUPPORTED;
+  }
+}
+
+ColView view_of(const ms_column* c) {
+  ColView v{};
+  v.format = c->fmt.format;
+  v.w = c->fmt.bit_width;
+  v.B = is_block(c->fmt.format) ? c->fmt.block_size : 1;
+  v.log2B = log2u(v.B);
+  v.n = c->n;
+  v.nb = c->n_blocks;
+  v.nrem = c->n_rem;
+  v.nruns = c->n_runs;
+  v.payload = c->payload;
+  v.cw = c->cw;
+  v.ref = c->ref;
+  v.rem = c->rem;
+  return v;
+}
+
+// RLE inputs need run starts (and the run covering each 2048-row chunk) to be
+// decoded tile by tile; both are transient scratch.
+struct RlePrep {
+  uint64_t starts = 0, chunk_run = 0, status = 0, ticket = 0;
+  bool used = false;
+};
+void plan_rle(Scratch& sc, const ms_column* c, RlePrep& p) {
+  if (!c || c->fmt.format != MS_RLE) return;
+  p.used = true;
+  p.starts = sc.add(8 * (c->n_runs + 1), false);
+  p.chunk_run = sc.add(4 * ((c->n + kChunk - 1) / kChunk + 1), false);
+  p.status = sc.add(8 * ((c->n_runs + kChunk - 1) / kChunk + 1), true);
+  p.ticket = sc.add(8, true);
+}
+cudaError_t run_rle(const Scratch& sc, const ms_column* c, const RlePrep& p, ColView& v, uint32_t* err) {
+  if (!p.used) return cudaSuccess;
+  uint64_t* starts = sc.at<uint64_t>(p.starts);
+  uint32_t* cr = sc.at<uint32_t>(p.chunk_run);
+  cudaError_t e = launch_rle_starts(c->payload, c->n_runs, c->n, starts, sc.at<uint64_t>(p.status),
+                                    sc.at<uint32_t>(p.ticket), err, sc.ctx.s);
+  if (e != cudaSuccess) return e;
+  e = launch_chunk_run(starts, c->n_runs, c->n, cr, sc.ctx.s);
+  v.run_starts = starts;
+  v.chunk_run = cr;
+  return e;
+}
+
+// Allocate an output column: one allocation, 256-byte aligned sections.
+ms_status alloc_column(const Ctx& ctx, ms_column* out, const ms_fmt& fmt, uint64_t n, uint64_t payload_cap_words,
+                       uint64_t n_runs) {
+  std::memset(out, 0, sizeof(*out));
+  out->fmt = fmt;
+  out->n = n;
+  uint64_t nb = 0, nrem = 0;
+  if (is_block(fmt.format)) {
+    nb = n / fmt.block_size;
+    nrem = n % fmt.block_size;
+  } else {
+    out->fmt.block_size = fmt.format == MS_STATIC_BP ? 0 : fmt.block_size;
+  }
+  out->n_blocks = nb;
+  out->n_rem = nrem;
+  out->n_runs = n_runs;
+  const uint64_t o_pay = 0;
+  uint64_t sz = align_up(8 * payload_cap_words);
+  uint64_t o_cw = sz, o_ref = sz, o_rem = sz;
+  if (is_block(fmt.format)) {
+    o_cw = sz;
+    sz = align_up(sz + 4 * (nb + 1));
+    o_ref = sz;
+    if (fmt.format != MS_DYN_BP) sz = align_up(sz + 8 * nb);
+    o_rem = sz;
+    sz = align_up(sz + 8 * nrem);
+  }
+  char* base = (char*)ctx.alloc(sz);
+  if (!base) return MS_E_NOMEM;
+  out->alloc = base;
+  out->alloc_bytes = sz;
+  out->payload = (uint64_t*)(base + o_pay);
+  if (is_block(fmt.format)) {
+    out->cw = (uint32_t*)(base + o_cw);
+    out->ref = fmt.format != MS_DYN_BP ? (uint64_t*)(base + o_ref) : nullptr;
+    out->rem = (uint64_t*)(base + o_rem);
+  }
+  return MS_OK;
+}
+
+void release(const Ctx& ctx, ms_column* c) {
+  if (c && c->alloc) ctx.free(c->alloc);
+  if (c) std::memset(c, 0, sizeof(*c));
+}
+
+OutView out_view(ms_column* o, uint64_t* status, uint32_t* ticket) {
+  OutView v{};
+  v.format = o->fmt.format;
+  v.w = o->fmt.bit_width;
+  v.B = is_block(o->fmt.format) ? o->fmt.block_size : 1;
+  v.log2B = log2u(v.B);
+  v.n = o->n;
+  v.n_dev = nullptr;
+  v.payload = o->payload;
+  v.cw = o->cw;
+  v.ref = o->ref;
+  v.rem = o->rem;
+  v.status = status;
+  v.ticket = ticket;
+  return v;
+}
+
+// Copy a column whose payload was over-allocated into an exact-size allocation
+// when asked to (MS_FLAG_SHRINK) or when more than 1 GiB would be wasted.
+ms_status maybe_shrink(const Ctx& ctx, ms_column* out) {
+  const uint64_t need = align_up(8 * out->payload_words);
+  const uint64_t have = (uint64_t)((char*)(out->cw ? (void*)out->cw : (void*)nullptr) - (char*)out->payload);
+  const bool force = ctx.c && (ctx.c->flags & MS_FLAG_SHRINK);
+  if (!out->cw || have <= need) return MS_OK;
+  if (!force && have - need < (1ull << 30)) return MS_OK;
+  ms_column t;
+  MS_TRY(alloc_column(ctx, &t, out->fmt, out->n, out->payload_words, out->n_runs));
+  t.payload_words = out->payload_words;
+  MS_TRY_CUDA(cudaMemcpyAsync(t.payload, out->payload, 8 * out->payload_words, cudaMemcpyDeviceToDevice, ctx.s));
+  MS_TRY_CUDA(cudaMemcpyAsync(t.cw, out->cw, 4 * (out->n_blocks + 1), cudaMemcpyDeviceToDevice, ctx.s));
+  if (out->ref && out->n_blocks)
+    MS_TRY_CUDA(cudaMemcpyAsync(t.ref, out->ref, 8 * out->n_blocks, cudaMemcpyDeviceToDevice, ctx.s));
+  if (out->n_rem) MS_TRY_CUDA(cudaMemcpyAsync(t.rem, out->rem, 8 * out->n_rem, cudaMemcpyDeviceToDevice, ctx.s));
+  release(ctx, out);
+  *out = t;
+  return MS_OK;
+}
+
+// Read back `count` u64 slots from device into host, synchronise, decode errors.
+ms_status readback(const Ctx& ctx, const uint64_t* dev, uint64_t* host, size_t count) {
+  if (count) MS_TRY_CUDA(cudaMemcpyAsync(host, dev, 8 * count, cudaMemcpyDeviceToHost, ctx.s));
+  MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  MS_TRY_CUDA(cudaGetLastError());
+  return MS_OK;
+}
+
+// finish a block-format output: read cw[nb] and the error word
+ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev) {
+  uint64_t h[2] = {0, 0};
+  MS_TRY_CUDA(cudaMemcpyAsync(&h[0], err_dev, 4, cudaMemcpyDeviceToHost, ctx.s));
+  if (is_block(out->fmt.format))
+    MS_TRY_CUDA(cudaMemcpyAsync(&h[1], out->cw + out->n_blocks, 4, cudaMemcpyDeviceToHost, ctx.s));
+  MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  MS_TRY_CUDA(cudaGetLastError());
+  const ms_status st = status_from_bits((uint32_t)h[0]);
+  if (st != MS_OK) return st;
+  if (is_block(out->fmt.format)) {
+    if (out->n_blocks == 0) h[1] = 0;
+    out->payload_words = (uint32_t)h[1] * (uint64_t)(out->fmt.block_size / 64);
+  }
+  return MS_OK;
+}
+
+uint32_t* sticky_err() {
+  static uint32_t* p[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!p[dev]) cudaGetSymbolAddress((void**)&p[dev], g_ms_sticky_err);
+  return p[dev];
+}
+
+// predicate in range form: keep = ((v - lo) <= span) != neg (D-11)
+ms_status make_pred(const ms_pred* p, PredSpec& ps) {
+  std::memset(&ps, 0, sizeof(ps));
+  const uint64_t MAX = ~0ull;
+  auto range = [&](uint64_t lo, uint64_t hi) { ps.lo = lo; ps.span = hi - lo; ps.neg = 0; };
+  auto none = [&]() { ps.lo = 0; ps.span = MAX; ps.neg = 1; };
+  switch (p->op) {
+    case MS_EQ: range(p->a, p->a); break;
+    case MS_NE: range(p->a, p->a); ps.neg = 1; break;
+    case MS_LT: if (p->a == 0) none(); else range(0, p->a - 1); break;
+    case MS_LE: range(0, p->a); break;
+    case MS_GT: if (p->a == MAX) none(); else range(p->a + 1, MAX); break;
+    case MS_GE: range(p->a, MAX); break;
+    case MS_BETWEEN: if (p->b <= p->a) none(); else range(p->a, p->b - 1); break;
+    case MS_IN_BITMAP:
+      if (!p->bitmap && p->bitmap_bits) return MS_E_INVALID;
+      ps.is_bitmap = 1;
+      ps.bitmap = p->bitmap;
+      ps.bitmap_bits = p->bitmap_bits;
+      break;
+    default:
+      return MS_E_INVALID;
+  }
+  return MS_OK;
+}
+
+bool same_fmt(const ms_fmt& a, const ms_fmt& b) {
+  if (a.format != b.format) return false;
+  if (a.format == MS_STATIC_BP) return a.bit_width == b.bit_width;
+  if (is_block(a.format)) return a.block_size == b.block_size;
+  return true;
+}
+
+// ------------------------------------------------------------ op bodies
+// Encode a source (described by launch functor) into fmt; shared by compress,
+// morph and project. n_out is host-known. `launch(out_view)` enqueues the engine.
+template <class Launch>
+ms_status encode_into(const Ctx& ctx, Scratch& sc, uint64_t meta_off, uint64_t st_off, uint64_t tk_off,
+                      uint64_t tk2_off, ms_fmt fmt, uint64_t n, uint64_t payload_cap_words, Launch launch,
+                      ms_column* out) {
+  uint32_t* err = sc.at<uint32_t>(meta_off);
+  if (fmt.format == MS_STATIC_BP && fmt.bit_width == 0) {  // auto width: max pass first
+    OutView mv{};
+    mv.format = OUT_MAX_ONLY;
+    mv.n = n;
+    mv.ticket = sc.at<uint32_t>(tk2_off);
+    mv.max_out = sc.at<unsigned long long>(meta_off + 8);
+    MS_TRY_CUDA(launch(mv));
+    uint64_t h[2];
+    MS_TRY(readback(ctx, sc.at<uint64_t>(meta_off), h, 2));
+    MS_TRY(status_from_bits((uint32_t)h[0]));
+    fmt.bit_width = ebw_host(h[1]) ? ebw_host(h[1]) : 1;
+  }
+  uint64_t cap = payload_cap_words;
+  if (fmt.format == MS_STATIC_BP) cap = words_for(n, fmt.bit_width);
+  if (fmt.format == MS_UNCOMPR) cap = n;
+  MS_TRY(alloc_column(ctx, out, fmt, n, cap, 0));
+  if (fmt.format == MS_UNCOMPR) out->payload_words = n;
+  if (fmt.format == MS_STATIC_BP) out->payload_words = cap;
+  if (is_block(fmt.format)) MS_TRY_CUDA(cudaMemsetAsync(out->cw, 0, 4, ctx.s));  // cw[0] = 0 even when n = 0
+  OutView ov = out_view(out, sc.at<uint64_t>(st_off), sc.at<uint32_t>(tk_off));
+  cudaError_t e = launch(ov);
+  if (e != cudaSuccess) {
+    release(ctx, out);
+    return cuda_status(e);
+  }
+  ms_status st = finish_output(ctx, out, err);
+  if (st == MS_OK) st = maybe_shrink(ctx, out);
+  if (st != MS_OK) release(ctx, out);
+  return st;
+}
+
+// RLE compression of raw device values: count run starts per tile,
+// scan, write (value, start), then lengths from consecutive starts.
+ms_status compress_rle(const Ctx& ctx, const uint64_t* values, uint64_t n, ms_column* out) {
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_cnt = sc.add(4 * (T + 1), false);
+  const uint64_t o_off = sc.add(8 * (T + 1), true);
+  const uint64_t o_st = sc.add(8 * ((T + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk = sc.add(8, true);
+  if (!sc.commit()) return MS_E_NOMEM;
+  MS_TRY_CUDA(launch_rle_count(values, n, sc.at<uint32_t>(o_cnt), ctx.s));
+  MS_TRY_CUDA(launch_count_scan(sc.at<uint32_t>(o_cnt), T, sc.at<uint64_t>(o_off), sc.at<uint64_t>(o_st),
+                                sc.at<uint32_t>(o_tk), ctx.s));
+  uint64_t R = 0;
+  MS_TRY(readback(ctx, sc.at<uint64_t>(o_off) + T, &R, 1));
+  ms_fmt f{MS_RLE, 0, 0, 0};
+  MS_TRY(alloc_column(ctx, out, f, n, 2 * R, R));
+  out->payload_words = 2 * R;
+  uint64_t* starts = (uint64_t*)ctx.alloc(8 * (R + 1));
+  if (!starts) {
+    release(ctx, out);
+    return MS_E_NOMEM;
+  }
+  cudaError_t e = launch_rle_write(values, n, sc.at<uint64_t>(o_off), out->payload, starts, ctx.s);
+  if (e == cudaSuccess) e = launch_rle_len(starts, R, n, out->payload, ctx.s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.s);
+  ctx.free(starts);
+  if (e != cudaSuccess) {
+    release(ctx, out);
+    return cuda_status(e);
+  }
+  return MS_OK;
+}
+
+// worst-case payload words of a block-format column of n values when every
+// block may need 64 bits
+uint64_t full_cap(uint64_t n, uint32_t B) { return (n / B) * B; }
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+int ms_abi_version(void) { return MS_ABI_VERSION; }
+uint64_t ms_launch_count(void) { return launch_count(); }
+
+const char* ms_status_str(ms_status s) {
+  switch (s) {
+    case MS_OK: return "MS_OK";
+    case MS_E_INVALID: return "MS_E_INVALID";
+    case MS_E_WIDTH_OVERFLOW: return "MS_E_WIDTH_OVERFLOW";
+    case MS_E_UNSUPPORTED: return "MS_E_UNSUPPORTED";
+    case MS_E_RANGE: return "MS_E_RANGE";
+    case MS_E_CORRUPT: return "MS_E_CORRUPT";
+    case MS_E_NOMEM: return "MS_E_NOMEM";
+    case MS_E_CUDA: return "MS_E_CUDA";
+  }
+  return "MS_E_UNKNOWN";
+}
+
+uint64_t ms_column_bytes(const ms_column* c) {
+  if (!c) return 0;
+  uint64_t b = 8 * c->payload_words;
+  if (is_block(c->fmt.format)) {
+    b += 4 * (c->n_blocks + 1) + 8 * c->n_rem;
+    if (c->fmt.format != MS_DYN_BP) b += 8 * c->n_blocks;
+  }
+  return b;
+}
+
+void ms_column_release(const ms_ctx* ctx, ms_column* col) { release(Ctx(ctx), col); }
+
+ms_status ms_compress(const ms_ctx* ctx_, const uint64_t* values, uint64_t n, ms_fmt fmt, ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_fmt(fmt));
+  if (n && !values) return MS_E_INVALID;
+  Ctx ctx(ctx_);
+  if (is_block(fmt.format) && 64 * (n / fmt.block_size) > 0xffffffffull) return MS_E_INVALID;  // D-4
+  if (fmt.format == MS_RLE) return compress_rle(ctx, values, n, out);
+  ms_column in{};
+  in.fmt = ms_fmt{MS_UNCOMPR, 0, 0, 0};
+  in.n = n;
+  in.payload_words = n;
+  in.payload = const_cast<uint64_t*>(values);
+  const ColView src = view_of(&in);
+  const uint64_t items = (n + kChunk - 1) / kChunk;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_st = sc.add(8 * (items + 1), true);
+  const uint64_t o_tk = sc.add(8, true);
+  const uint64_t o_tk2 = sc.add(8, true);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  auto launch = [&](const OutView& ov) { return launch_engine_col(src, ov, err, ctx.s); };
+  return encode_into(ctx, sc, o_meta, o_st, o_tk, o_tk2, fmt, n,
+                     is_block(fmt.format) ? full_cap(n, fmt.block_size) : 0, launch, out);
+}
+
+ms_status ms_decompress(const ms_ctx* ctx_, const ms_column* in, uint64_t* values) {
+  MS_TRY(check_col(in));
+  if (in->n && !values) return MS_E_INVALID;
+  if (in->n == 0) return MS_OK;
+  Ctx ctx(ctx_);
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_tk = sc.add(8, true);
+  RlePrep rp;
+  plan_rle(sc, in, rp);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView src = view_of(in);
+  MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+  ms_column o{};
+  o.fmt = ms_fmt{MS_UNCOMPR, 0, 0, 0};
+  o.n = in->n;
+  o.payload = values;
+  OutView ov = out_view(&o, nullptr, sc.at<uint32_t>(o_tk));
+  MS_TRY_CUDA(launch_engine_col(src, ov, err, ctx.s));
+  uint64_t h = 0;
+  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), &h, 1));
+  return status_from_bits((uint32_t)h);
+}
+
+ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(in));
+  MS_TRY(check_fmt(fmt));
+  Ctx ctx(ctx_);
+  const uint64_t n = in->n;
+  if (is_block(fmt.format) && 64 * (n / fmt.block_size) > 0xffffffffull) return MS_E_INVALID;
+  if (same_fmt(in->fmt, fmt)) {  // identity morph: byte-identical
+    MS_TRY(alloc_column(ctx, out, in->fmt, n, in->payload_words, in->n_runs));
+    out->payload_words = in->payload_words;
+    if (in->payload_words)
+      MS_TRY_CUDA(cudaMemcpyAsync(out->payload, in->payload, 8 * in->payload_words, cudaMemcpyDeviceToDevice, ctx.s));
+    if (is_block(fmt.format)) {
+      MS_TRY_CUDA(cudaMemcpyAsync(out->cw, in->cw, 4 * (in->n_blocks + 1), cudaMemcpyDeviceToDevice, ctx.s));
+      if (out->ref && in->n_blocks)
+        MS_TRY_CUDA(cudaMemcpyAsync(out->ref, in->ref, 8 * in->n_blocks, cudaMemcpyDeviceToDevice, ctx.s));
+      if (in->n_rem)
+        MS_TRY_CUDA(cudaMemcpyAsync(out->rem, in->rem, 8 * in->n_rem, cudaMemcpyDeviceToDevice, ctx.s));
+    }
+    return MS_OK;
+  }
+  if (fmt.format == MS_RLE) {  // staged through an uncompressed buffer
+    uint64_t* tmp = (uint64_t*)ctx.alloc(8 * (n ? n : 1));
+    if (!tmp) return MS_E_NOMEM;
+    ms_status st = ms_decompress(ctx_, in, tmp);
+    if (st == MS_OK) st = compress_rle(ctx, tmp, n, out);
+    ctx.free(tmp);
+    return st;
+  }
+  const uint64_t items = (n + kChunk - 1) / kChunk;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_st = sc.add(8 * (items + 1), true);
+  const uint64_t o_tk = sc.add(8, true);
+  const uint64_t o_tk2 = sc.add(8, true);
+  RlePrep rp;
+  plan_rle(sc, in, rp);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView src = view_of(in);
+  MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+  auto launch = [&](const OutView& ov) { return launch_engine_col(src, ov, err, ctx.s); };
+  return encode_into(ctx, sc, o_meta, o_st, o_tk, o_tk2, fmt, n,
+                     is_block(fmt.format) ? full_cap(n, fmt.block_size) : 0, launch, out);
+}
+
+ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred, uint64_t row_offset,
+                    ms_fmt out_fmt, ms_column* out) {
+  if (!out || !pred) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(in));
+  MS_TRY(check_fmt(out_fmt));
+  PredSpec ps;
+  MS_TRY(make_pred(pred, ps));
+  Ctx ctx(ctx_);
+  const uint64_t n = in->n;
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  const uint64_t n_words = T * (kChunk / 32);
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] max position
+  const uint64_t o_bits = sc.add(4 * n_words, false);
+  const uint64_t o_cnt = sc.add(4 * (T + 1), false);
+  const uint64_t o_last = sc.add(4 * (T + 1), false);
+  const uint64_t o_off = sc.add(8 * (T + 1), true);
+  const uint64_t o_start = sc.add(4 * (T + 1), false);
+  const uint64_t o_st1 = sc.add(8 * ((T + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk1 = sc.add(8, true);
+  const uint64_t o_st2 = sc.add(8 * (T + 1), true);
+  const uint64_t o_tk2 = sc.add(8, true);
+  RlePrep rp;
+  plan_rle(sc, in, rp);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView src = view_of(in);
+  MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+  uint64_t* tile_off = sc.at<uint64_t>(o_off);
+  MS_TRY_CUDA(launch_select_tiles(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_cnt), sc.at<uint32_t>(o_last),
+                                  T, ctx.s));
+  MS_TRY_CUDA(launch_tile_scan(sc.at<uint32_t>(o_cnt), sc.at<uint32_t>(o_last), T, row_offset, tile_off,
+                               sc.at<uint32_t>(o_start), sc.at<unsigned long long>(o_meta + 8),
+                               sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1), ctx.s));
+  uint64_t h[3] = {0, 0, 0};
+  if (T) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], tile_off + T, 8, cudaMemcpyDeviceToHost, ctx.s));
+  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
+  MS_TRY(status_from_bits((uint32_t)h[0]));
+  const uint64_t n_out = T ? h[2] : 0;
+  const uint64_t max_pos = h[1];
+  // size the output (n_out and the largest position are known now)
+  uint64_t cap = 0;
+  ms_fmt f = out_fmt;
+  switch (f.format) {
+    case MS_UNCOMPR: cap = n_out; break;
+    case MS_RLE: cap = 2 * n_out; break;
+    case MS_STATIC_BP: {
+      const uint32_t need = n_out ? (ebw_host(max_pos) ? ebw_host(max_pos) : 1) : 1;
+      if (f.bit_width == 0) f.bit_width = need;
+      else if (n_out && ebw_host(max_pos) > f.bit_width) return MS_E_WIDTH_OVERFLOW;
+      cap = words_for(n_out, f.bit_width);
+      break;
+    }
+    default: {
+      const uint32_t B = f.block_size;
+      const uint64_t nb = n_out / B;
+      uint64_t wsum = 64 * nb;
+      if (f.format == MS_DYN_BP) {
+        wsum = nb * ebw_host(max_pos);
+      } else if (nb) {  // sum_k ebw(span_k) <= nb (1 + log2(n / nb)) (Jensen)
+        const uint64_t q = (n + nb - 1) / nb;
+        const uint64_t lg = q > 1 ? 64 - __builtin_clzll(q - 1) : 0;
+        wsum = nb * (1 + lg);
+        if (wsum > 64 * nb) wsum = 64 * nb;
+      }
+      cap = wsum * (B / 64);
+    }
+  }
+  if (is_block(f.format) && 64 * (n_out / f.block_size) > 0xffffffffull) return MS_E_INVALID;
+  MS_TRY(alloc_column(ctx, out, f, n_out, cap, f.format == MS_RLE ? n_out : 0));
+  if (f.format == MS_UNCOMPR || f.format == MS_RLE || f.format == MS_STATIC_BP) out->payload_words = cap;
+  if (n_out) {
+    OutView ov = out_view(out, sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2));
+    cudaError_t e = launch_engine_bitmask(sc.at<uint32_t>(o_bits), tile_off, sc.at<uint32_t>(o_start), n_words,
+                                          row_offset, ov, err, ctx.s);
+    if (e != cudaSuccess) {
+      release(ctx, out);
+      return cuda_status(e);
+    }
+  } else if (is_block(f.format)) {
+    cudaMemsetAsync(out->cw, 0, 4, ctx.s);
+  }
+  ms_status st = finish_output(ctx, out, err);
+  if (st == MS_OK) st = maybe_shrink(ctx, out);
+  if (st != MS_OK) release(ctx, out);
+  return st;
+}
+
+ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column* positions, uint64_t row_offset,
+                     ms_fmt out_fmt, ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(data));
+  MS_TRY(check_col(positions));
+  MS_TRY(check_fmt(out_fmt));
+  if (out_fmt.format == MS_RLE) return MS_E_UNSUPPORTED;
+  Ctx ctx(ctx_);
+  const uint64_t n = positions->n;
+  if (is_block(out_fmt.format) && 64 * (n / out_fmt.block_size) > 0xffffffffull) return MS_E_INVALID;
+  const uint64_t items = (n + kChunk - 1) / kChunk;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_st = sc.add(8 * (items + 1), true);
+  const uint64_t o_tk = sc.add(8, true);
+  const uint64_t o_tk2 = sc.add(8, true);
+  RlePrep rp_pos, rp_data;
+  plan_rle(sc, positions, rp_pos);
+  plan_rle(sc, data, rp_data);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView pv = view_of(positions), dv = view_of(data);
+  MS_TRY_CUDA(run_rle(sc, positions, rp_pos, pv, err));
+  MS_TRY_CUDA(run_rle(sc, data, rp_data, dv, err));
+  auto launch = [&](const OutView& ov) { return launch_engine_gather(pv, dv, row_offset, ov, err, ctx.s); };
+  uint64_t cap = 0;
+  if (is_block(out_fmt.format)) {
+    uint32_t wmax = 64;  // projected codes cannot be wider than a static data width
+    if (data->fmt.format == MS_STATIC_BP && out_fmt.format != MS_DELTA_BP) wmax = data->fmt.bit_width;
+    cap = (n / out_fmt.block_size) * (out_fmt.block_size / 64) * wmax;
+  }
+  return encode_into(ctx, sc, o_meta, o_st, o_tk, o_tk2, out_fmt, n, cap, launch, out);
+}
+
+ms_status ms_agg_sum(const ms_ctx* ctx_, const ms_column* in, const ms_column* positions, uint64_t row_offset,
+                     uint64_t* sum) {
+  MS_TRY(check_col(in));
+  if (positions) MS_TRY(check_col(positions));
+  if (!sum) return MS_E_INVALID;
+  Ctx ctx(ctx_);
+  MS_TRY_CUDA(cudaMemsetAsync(sum, 0, 8, ctx.s));
+  uint32_t* err = sticky_err();
+  const bool need_rle = in->fmt.format == MS_RLE || (positions && positions->fmt.format == MS_RLE);
+  if (!need_rle) {
+    if (positions)
+      MS_TRY_CUDA(launch_sum_at(view_of(in), view_of(positions), row_offset, (unsigned long long*)sum, err, ctx.s));
+    else if (in->n)
+      MS_TRY_CUDA(launch_sum(view_of(in), (unsigned long long*)sum, err, ctx.s));
+    return MS_OK;
+  }
+  Scratch sc(ctx);
+  RlePrep rp_in, rp_pos;
+  plan_rle(sc, in, rp_in);
+  plan_rle(sc, positions, rp_pos);
+  if (!sc.commit()) return MS_E_NOMEM;
+  ColView iv = view_of(in);
+  MS_TRY_CUDA(run_rle(sc, in, rp_in, iv, err));
+  if (positions) {
+    ColView pv = view_of(positions);
+    MS_TRY_CUDA(run_rle(sc, positions, rp_pos, pv, err));
+    MS_TRY_CUDA(launch_sum_at(iv, pv, row_offset, (unsigned long long*)sum, err, ctx.s));
+  } else if (in->n) {
+    MS_TRY_CUDA(launch_sum(iv, (unsigned long long*)sum, err, ctx.s));
+  }
+  return MS_OK;  // scratch is freed stream-ordered after the kernels
+}
+
+ms_status ms_agg_sum_grouped(const ms_ctx* ctx_, const ms_column* gid, const ms_column* vals, uint64_t n_groups,
+                             uint64_t* sums) {
+  MS_TRY(check_col(gid));
+  MS_TRY(check_col(vals));
+  if (gid->n != vals->n) return MS_E_INVALID;  // LengthMismatch
+  if (n_groups && !sums) return MS_E_INVALID;
+  Ctx ctx(ctx_);
+  if (n_groups) MS_TRY_CUDA(cudaMemsetAsync(sums, 0, 8 * n_groups, ctx.s));
+  if (gid->n == 0) return MS_OK;
+  uint32_t* err = sticky_err();
+  Scratch sc(ctx);
+  RlePrep rp_g, rp_v;
+  plan_rle(sc, gid, rp_g);
+  plan_rle(sc, vals, rp_v);
+  if (!sc.commit()) return MS_E_NOMEM;
+  ColView gv = view_of(gid), vv = view_of(vals);
+  MS_TRY_CUDA(run_rle(sc, gid, rp_g, gv, err));
+  MS_TRY_CUDA(run_rle(sc, vals, rp_v, vv, err));
+  MS_TRY_CUDA(launch_sum_grouped(gv, vv, n_groups, (unsigned long long*)sums, err, ctx.s));
+  return MS_OK;
+}
+
+ms_status ms_column_to_device(const ms_ctx* ctx_, const ms_column* h, ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(h));
+  Ctx ctx(ctx_);
+  MS_TRY(alloc_column(ctx, out, h->fmt, h->n, h->payload_words, h->n_runs));
+  out->payload_words = h->payload_words;
+  auto cp = [&](void* d, const void* s, uint64_t bytes) {
+    return bytes ? cudaMemcpyAsync(d, s, bytes, cudaMemcpyHostToDevice, ctx.s) : cudaSuccess;
+  };
+  cudaError_t e = cp(out->payload, h->payload, 8 * h->payload_words);
+  if (e == cudaSuccess && is_block(h->fmt.format)) {
+    e = cp(out->cw, h->cw, 4 * (h->n_blocks + 1));
+    if (e == cudaSuccess && out->ref) e = cp(out->ref, h->ref, 8 * h->n_blocks);
+    if (e == cudaSuccess) e = cp(out->rem, h->rem, 8 * h->n_rem);
+  }
+  if (e != cudaSuccess) {
+    release(ctx, out);
+    return cuda_status(e);
+  }
+  return MS_OK;
+}
+
+ms_status ms_column_to_host(const ms_ctx* ctx_, const ms_column* d, ms_column* h) {
+  MS_TRY(check_col(d));
+  if (!h) return MS_E_INVALID;
+  Ctx ctx(ctx_);
+  auto cp = [&](void* dst, const void* s, uint64_t bytes) {
+    if (!bytes) return cudaSuccess;
+    if (!dst) return cudaErrorInvalidValue;
+    return cudaMemcpyAsync(dst, s, bytes, cudaMemcpyDeviceToHost, ctx.s);
+  };
+  MS_TRY_CUDA(cp(h->payload, d->payload, 8 * d->payload_words));
+  if (is_block(d->fmt.format)) {
+    MS_TRY_CUDA(cp(h->cw, d->cw, 4 * (d->n_blocks + 1)));
+    if (d->ref) MS_TRY_CUDA(cp(h->ref, d->ref, 8 * d->n_blocks));
+    MS_TRY_CUDA(cp(h->rem, d->rem, 8 * d->n_rem));
+  }
+  MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  h->fmt = d->fmt;
+  h->n = d->n;
+  h->n_blocks = d->n_blocks;
+  h->n_rem = d->n_rem;
+  h->n_runs = d->n_runs;
+  h->payload_words = d->payload_words;
+  h->alloc = nullptr;
+  h->alloc_bytes = 0;
+  return MS_OK;
+}
+
+ms_status ms_check_errors(const ms_ctx* ctx_) {
+  Ctx ctx(ctx_);
+  uint32_t h = 0;
+  uint32_t* p = sticky_err();
+  MS_TRY_CUDA(cudaMemcpyAsync(&h, p, 4, cudaMemcpyDeviceToHost, ctx.s));
+  MS_TRY_CUDA(cudaMemsetAsync(p, 0, 4, ctx.s));
+  MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  MS_TRY_CUDA(cudaGetLastError());
+  return status_from_bits(h);
+}
+
+}  // extern "C"

@@ -1,0 +1,286 @@
+// common.cuh — device building blocks of libms (sm_100a).
+//
+// The paper's operator is three layers: a column layer (host
+// launcher: main part / remainder split, sizes, allocation), a buffer layer
+// (format-specific decompression on the input side, compression on the output
+// side) and a vector-register layer (the operator core). On the GPU:
+//   buffer layer  -> CTA-cooperative tile decoders/encoders over a shared-memory
+//                    tile of 2048 rows (the paper's 2048-element, 16 KiB
+//                    output buffer, is the same size by design);
+//   register core -> per-thread predicate / gather / accumulate, warp ballot +
+//                    popc compaction (the "bit mask" of P:484-486).
+// Device-wide prefixes (output offsets, cumulative widths) use a decoupled
+// look-back over work items taken in order from an atomic ticket.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ms.h"
+
+namespace ms {
+
+constexpr int kChunk = 2048;               // rows per work item / tile
+constexpr int kThreads = 256;              // CTA size of the generic engine
+constexpr int kVPT = kChunk / kThreads;    // 8 values per thread
+constexpr int kMaxBlocksPerChunk = kChunk / 128;
+constexpr unsigned kFull = 0xffffffffu;
+
+// device error bits: bit s <=> ms_status s
+__host__ __device__ constexpr uint32_t err_bit(int s) { return 1u << s; }
+
+// ---------------------------------------------------------------- views
+// A column as kernels see it (by value in kernel parameters).
+struct ColView {
+  int32_t format;
+  uint32_t w;          // STATIC_BP width
+  uint32_t B;          // block size (block formats)
+  uint32_t log2B;
+  uint64_t n, nb, nrem, nruns;
+  const uint64_t* payload;
+  const uint32_t* cw;
+  const uint64_t* ref;
+  const uint64_t* rem;
+  const uint64_t* run_starts;  // RLE: exclusive prefix of run lengths, nruns+1 entries (scratch)
+  const uint32_t* chunk_run;   // RLE: index of the run covering row 2048*c (scratch)
+};
+
+// ------------------------------------------------------------ bit helpers
+// effective bit width: 0 for 0, else index of highest set bit + 1
+__device__ __forceinline__ uint32_t ebw64(uint64_t x) { return 64u - (uint32_t)__clzll((long long)x); }
+
+__device__ __forceinline__ uint64_t low_mask(uint32_t w) { return w >= 64 ? ~0ull : ((1ull << w) - 1); }
+
+// value at stream bit `bit`, width w (0..64), LSB-first uint64 words (D-1)
+__device__ __forceinline__ uint64_t unpack_at(const uint64_t* __restrict__ p, uint64_t bit, uint32_t w) {
+  if (w == 0) return 0;
+  const uint64_t word = bit >> 6;
+  const uint32_t s = (uint32_t)(bit & 63);
+  uint64_t v = __ldg(p + word) >> s;
+  if (s + w > 64) v |= __ldg(p + word + 1) << (64 - s);
+  return v & low_mask(w);
+}
+
+// volatile 64-bit status words (single-copy atomic when aligned)
+__device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
+  return *reinterpret_cast<const volatile uint64_t*>(p);
+}
+__device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
+  *reinterpret_cast<volatile uint64_t*>(p) = v;
+}
+
+// ------------------------------------------------------------ scans
+__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t t = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t t = __shfl_xor_sync(kFull, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+
+// CTA-wide exclusive scan (kThreads threads). sm must hold >= 10 uint64.
+// Returns the exclusive prefix; *total gets the CTA total. Ends with a barrier.
+__device__ __forceinline__ uint64_t cta_excl_scan(uint64_t v, uint64_t* sm, uint64_t* total) {
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t inc = warp_incl_scan(v);
+  if (lane == 31) sm[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t x = lane < kWarps ? sm[lane] : 0;
+    uint64_t xi = warp_incl_scan(x);
+    if (lane < kWarps) sm[lane] = xi - x;
+    if (lane == kWarps - 1) sm[kWarps] = xi;
+  }
+  __syncthreads();
+  const uint64_t ex = sm[wid] + inc - v;
+  if (total) *total = sm[kWarps];
+  __syncthreads();
+  return ex;
+}
+
+// ------------------------------------------------------- decoupled look-back
+// status word: [63:62] flag (0 invalid, 1 aggregate, 2 inclusive prefix),
+// [61:0] value. Items are taken in increasing order from an atomic ticket, so
+// every item only waits on items that are already being processed by resident
+// CTAs (no deadlock).
+constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+// Call with ALL 32 lanes of ONE warp. Returns the exclusive prefix of item t.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, uint64_t t, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) {
+    if (lane == 0) st_volatile(&status[0], kFlagP | agg);
+    return 0;
+  }
+  if (lane == 0) st_volatile(&status[t], kFlagA | agg);
+  uint64_t excl = 0;
+  int64_t base = (int64_t)t - 1;
+  while (true) {
+    const int64_t idx = base - lane;
+    uint64_t s = kFlagP;  // before item 0: prefix 0
+    if (idx >= 0) {
+      int spins = 0;
+      while (((s = ld_volatile(&status[idx])) >> 62) == 0) {
+        if (++spins > 8) __nanosleep(64);
+      }
+    }
+    const unsigned pmask = __ballot_sync(kFull, (s >> 62) == 2);
+    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
+    uint64_t v = (lane <= first_p) ? (s & kValMask) : 0;
+    excl += warp_sum(v);
+    if (pmask) break;
+    base -= 32;
+  }
+  if (lane == 0) st_volatile(&status[t], kFlagP | ((excl + agg) & kValMask));
+  return excl;
+}
+
+// ---------------------------------------------------------- random access
+// value at row r of a column (r < c.n). O(1) for UNCOMPR, STATIC_BP, DYN_BP,
+// FOR_BP (cw / ref headers, D-12); O(B) for DELTA_BP (prefix inside the
+// block); O(log R) for RLE (search of the run starts).
+__device__ __forceinline__ uint64_t read_row(const ColView& c, uint64_t r) {
+  switch (c.format) {
+    case MS_UNCOMPR:
+      return __ldg(c.payload + r);
+    case MS_STATIC_BP:
+      return unpack_at(c.payload, r * c.w, c.w);
+    case MS_DYN_BP:
+    case MS_FOR_BP:
+    case MS_DELTA_BP: {
+      if (r >= (c.nb << c.log2B)) return __ldg(c.rem + (r - (c.nb << c.log2B)));
+      const uint64_t b = r >> c.log2B;
+      const uint32_t j = (uint32_t)(r & (c.B - 1));
+      const uint32_t cw0 = __ldg(c.cw + b);
+      const uint32_t w = __ldg(c.cw + b + 1) - cw0;
+      const uint64_t bit0 = (uint64_t)cw0 * c.B;
+      if (c.format == MS_DYN_BP) return unpack_at(c.payload, bit0 + (uint64_t)j * w, w);
+      if (c.format == MS_FOR_BP) return __ldg(c.ref + b) + unpack_at(c.payload, bit0 + (uint64_t)j * w, w);
+      uint64_t v = __ldg(c.ref + b);
+      for (uint32_t q = 0; q <= j; ++q) v += unpack_at(c.payload, bit0 + (uint64_t)q * w, w);
+      return v;
+    }
+    case MS_RLE: {
+      uint64_t lo = 0, hi = c.nruns;  // find last k with starts[k] <= r
+      while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (__ldg(c.run_starts + mid) <= r) lo = mid; else hi = mid;
+      }
+      return __ldg(c.payload + 2 * lo);
+    }
+  }
+  return 0;
+}
+
+// -------------------------------------------------------- tile decoder
+// Shared memory of the generic engine.
+struct EngineSmem {
+  uint64_t vals[kChunk];
+  uint64_t ex[kThreads];
+  uint64_t scan[16];
+  uint64_t bmin[kMaxBlocksPerChunk], bmax[kMaxBlocksPerChunk], bex[kMaxBlocksPerChunk];
+  uint32_t bw[kMaxBlocksPerChunk];
+  uint32_t item;
+  uint32_t flag;
+  uint64_t aux;
+};
+
+// Decode rows [r0, r0+cnt) of column c into sm.vals (buffer layer, input side,
+// P:479-481). r0 is a multiple of kChunk (hence of every block size), cnt <= kChunk.
+// Ends with a barrier.
+__device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_t cnt, EngineSmem& sm) {
+  const int tid = threadIdx.x;
+  switch (c.format) {
+    case MS_UNCOMPR:
+      for (uint32_t i = tid; i < cnt; i += kThreads) sm.vals[i] = __ldg(c.payload + r0 + i);
+      break;
+    case MS_STATIC_BP:
+      for (uint32_t i = tid; i < cnt; i += kThreads) sm.vals[i] = unpack_at(c.payload, (r0 + i) * c.w, c.w);
+      break;
+    case MS_DYN_BP:
+    case MS_FOR_BP:
+      for (uint32_t i = tid; i < cnt; i += kThreads) sm.vals[i] = read_row(c, r0 + i);
+      break;
+    case MS_DELTA_BP: {
+      // thread t owns rows [8t, 8t+8): local prefix of the deltas, CTA scan,
+      // then subtract the prefix at the block head (segmented scan).
+      const uint32_t i0 = tid * kVPT;
+      const uint64_t r = r0 + i0;
+      const uint64_t main_rows = c.nb << c.log2B;
+      uint64_t loc[kVPT];
+      uint64_t tsum = 0;
+      const bool in_main = i0 < cnt && r < main_rows;
+      uint64_t b = 0;
+      if (in_main) {
+        b = r >> c.log2B;
+        const uint32_t j0 = (uint32_t)(r & (c.B - 1));
+        const uint32_t cw0 = __ldg(c.cw + b);
+        const uint32_t w = __ldg(c.cw + b + 1) - cw0;
+        const uint64_t bit0 = (uint64_t)cw0 * c.B + (uint64_t)j0 * w;
+#pragma unroll
+        for (int q = 0; q < kVPT; ++q) {
+          tsum += unpack_at(c.payload, bit0 + (uint64_t)q * w, w);
+          loc[q] = tsum;
+        }
+      }
+      const uint64_t ex = cta_excl_scan(in_main ? tsum : 0, sm.scan, nullptr);
+      sm.ex[tid] = ex;
+      __syncthreads();
+      if (in_main) {
+        const uint32_t head = (uint32_t)(((b << c.log2B) - r0) / kVPT);
+        const uint64_t base = __ldg(c.ref + b) + (ex - sm.ex[head]);
+#pragma unroll
+        for (int q = 0; q < kVPT; ++q) sm.vals[i0 + q] = base + loc[q];
+      } else {
+        for (int q = 0; q < kVPT; ++q)
+          if (i0 + q < cnt) sm.vals[i0 + q] = __ldg(c.rem + (r + q - main_rows));
+      }
+      break;
+    }
+    case MS_RLE: {
+      // mark run starts inside the chunk, scan the marks -> run index per row
+      const uint64_t k0 = __ldg(c.chunk_run + (r0 / kChunk));
+      const uint32_t i0 = tid * kVPT;
+      // reuse sm.vals as the mark array (1 = a run starts at this row, row > r0)
+      for (int q = 0; q < kVPT; ++q) sm.vals[i0 + q] = 0;
+      __syncthreads();
+      for (uint64_t k = k0 + 1 + tid;; k += kThreads) {
+        if (k >= c.nruns) break;
+        const uint64_t s = __ldg(c.run_starts + k);
+        if (s >= r0 + cnt) break;
+        sm.vals[s - r0] = 1;
+      }
+      __syncthreads();
+      uint64_t loc[kVPT];
+      uint64_t tsum = 0;
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        tsum += sm.vals[i0 + q];
+        loc[q] = tsum;
+      }
+      const uint64_t ex = cta_excl_scan(tsum, sm.scan, nullptr);
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q)
+        if (i0 + q < cnt) sm.vals[i0 + q] = __ldg(c.payload + 2 * (k0 + ex + loc[q]));
+      break;
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace ms

@@ -1,0 +1,238 @@
+// engine.cuh — the generic on-the-fly de/re-compression engine (P:297-337,
+// 468-505): a persistent kernel takes work items (2048 output rows) in order
+// from a ticket, fills a shared-memory tile from a Source (decode of a column,
+// expansion of a select bit mask, or a gather through positions), and encodes
+// the tile into the output format with the output-side buffer layer below.
+// Block formats need the exclusive prefix of the block widths (cw, D-4): it
+// comes from a decoupled look-back over the per-item width sums, so the whole
+// output is produced in one pass with one store per word.
+#pragma once
+#include "common.cuh"
+
+namespace ms {
+
+enum : int32_t { OUT_MAX_ONLY = 100 };  // pseudo-format: only reduce the max (auto static width)
+
+struct OutView {
+  int32_t format;
+  uint32_t w;
+  uint32_t B;
+  uint32_t log2B;
+  uint64_t n;                // logical length if n_dev == nullptr
+  const uint64_t* n_dev;     // device-resident logical length (select outputs)
+  uint64_t* payload;
+  uint32_t* cw;
+  uint64_t* ref;
+  uint64_t* rem;
+  uint64_t* status;          // look-back status, one per item
+  uint32_t* ticket;
+  unsigned long long* max_out;  // OUT_MAX_ONLY target
+};
+
+// Output word m (bits [64m, 64m+64)) of a packed stream of `cnt` codes of width
+// w (1..64); code(j) yields the j-th code, already < 2^w.
+template <class CodeFn>
+__device__ __forceinline__ uint64_t pack_word(CodeFn code, uint32_t cnt, uint32_t w, uint64_t m) {
+  const uint64_t bit0 = m * 64;
+  uint32_t j = (uint32_t)(bit0 / w);
+  const uint32_t s = (uint32_t)(bit0 - (uint64_t)j * w);
+  uint64_t acc = j < cnt ? code(j) >> s : 0;
+  for (++j; j < cnt; ++j) {
+    const uint64_t jb = (uint64_t)j * w;
+    if (jb >= bit0 + 64) break;
+    acc |= code(j) << (jb - bit0);
+  }
+  return acc;
+}
+
+// Output-side buffer layer: encode sm.vals[0..cnt) = rows
+// [r0, r0+cnt) of the output column. Item index = r0 / kChunk.
+__device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uint64_t r0, uint32_t cnt,
+                                            uint64_t n, EngineSmem& sm, uint32_t* err) {
+  const int tid = threadIdx.x;
+  switch (o.format) {
+    case MS_UNCOMPR:
+      for (uint32_t i = tid; i < cnt; i += kThreads) o.payload[r0 + i] = sm.vals[i];
+      return;
+    case MS_RLE:  // only for inputs without equal neighbours (select positions): runs of length 1
+      for (uint32_t i = tid; i < cnt; i += kThreads) {
+        o.payload[2 * (r0 + i)] = sm.vals[i];
+        o.payload[2 * (r0 + i) + 1] = 1;
+      }
+      return;
+    case OUT_MAX_ONLY: {
+      uint64_t mx = 0;
+      for (uint32_t i = tid; i < cnt; i += kThreads) mx = sm.vals[i] > mx ? sm.vals[i] : mx;
+      mx = warp_max(mx);
+      if ((tid & 31) == 0 && mx) atomicMax(o.max_out, (unsigned long long)mx);
+      return;
+    }
+    case MS_STATIC_BP: {
+      const uint32_t w = o.w;
+      if (w < 64)
+        for (uint32_t i = tid; i < cnt; i += kThreads)
+          if (sm.vals[i] >> w) atomicOr(err, err_bit(MS_E_WIDTH_OVERFLOW));
+      const uint64_t mask = low_mask(w);
+      const uint64_t wbase = (uint64_t)item * (kChunk / 64) * w;
+      const uint64_t nwords = ((uint64_t)cnt * w + 63) / 64;
+      auto code = [&](uint32_t j) { return sm.vals[j] & mask; };
+      for (uint64_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, cnt, w, m);
+      return;
+    }
+    default:
+      break;
+  }
+  // ---- block formats: DYN_BP / FOR_BP / DELTA_BP
+  const uint32_t B = o.B, lg = o.log2B;
+  const uint32_t nbc = cnt >> lg;  // full blocks in this tile (all but the last tile: kChunk/B)
+  const uint64_t kb0 = r0 >> lg;   // global index of the tile's first block
+  if (tid < kMaxBlocksPerChunk) {
+    sm.bmin[tid] = ~0ull;
+    sm.bmax[tid] = 0;
+  }
+  __syncthreads();
+  {
+    const uint32_t i0 = tid * kVPT;
+    if (i0 < (nbc << lg)) {
+      const uint32_t blk = i0 >> lg;
+      uint64_t lmin = ~0ull, lmax = 0;
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const uint32_t j = i0 + q;
+        uint64_t c;
+        if (o.format == MS_DELTA_BP) c = (j & (B - 1)) ? sm.vals[j] - sm.vals[j - 1] : 0;
+        else c = sm.vals[j];
+        lmin = c < lmin ? c : lmin;
+        lmax = c > lmax ? c : lmax;
+      }
+      if (o.format == MS_FOR_BP) atomicMin((unsigned long long*)&sm.bmin[blk], (unsigned long long)lmin);
+      atomicMax((unsigned long long*)&sm.bmax[blk], (unsigned long long)lmax);
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int lane = tid;
+    uint32_t w = 0;
+    if (lane < (int)nbc) {
+      w = o.format == MS_FOR_BP ? ebw64(sm.bmax[lane] - sm.bmin[lane]) : ebw64(sm.bmax[lane]);
+      sm.bw[lane] = w;
+    }
+    const uint64_t incl = warp_incl_scan(w);
+    const uint64_t tile_sum = __shfl_sync(kFull, incl, 31);
+    const uint64_t E = lookback_warp(o.status, item, tile_sum);
+    if (lane < (int)nbc) {
+      const uint64_t c_incl = E + incl;
+      if (c_incl > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      o.cw[kb0 + lane + 1] = (uint32_t)c_incl;
+      sm.bex[lane] = E + incl - w;
+      if (o.format == MS_FOR_BP) o.ref[kb0 + lane] = sm.bmin[lane];
+      if (o.format == MS_DELTA_BP) o.ref[kb0 + lane] = sm.vals[lane << lg];
+    }
+    if (item == 0 && lane == 0) o.cw[0] = 0;
+  }
+  __syncthreads();
+  for (uint32_t bi = 0; bi < nbc; ++bi) {
+    const uint32_t w = sm.bw[bi];
+    if (w == 0) continue;
+    const uint64_t* v = sm.vals + (bi << lg);
+    const uint64_t wbase = sm.bex[bi] * (B / 64);
+    const uint32_t nwords = (B / 64) * w;
+    if (o.format == MS_FOR_BP) {
+      const uint64_t rf = sm.bmin[bi];
+      auto code = [&](uint32_t j) { return v[j] - rf; };
+      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, B, w, m);
+    } else if (o.format == MS_DELTA_BP) {
+      auto code = [&](uint32_t j) { return j ? v[j] - v[j - 1] : 0ull; };
+      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, B, w, m);
+    } else {
+      auto code = [&](uint32_t j) { return v[j]; };
+      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, B, w, m);
+    }
+  }
+  const uint32_t rem_cnt = cnt - (nbc << lg);
+  if (rem_cnt) {  // the final partial block -> uncompressed remainder
+    for (uint32_t i = tid; i < rem_cnt; i += kThreads) o.rem[i] = sm.vals[(nbc << lg) + i];
+  }
+}
+
+// ------------------------------------------------------------------ sources
+// Decode of rows [r0, r0+cnt) of a column (compress / decompress / morph).
+struct ColSource {
+  ColView c;
+  __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, EngineSmem& sm, uint32_t* err) const {
+    load_rows(c, r0, cnt, sm);
+  }
+};
+
+// Expansion of the select bit mask into positions (ranks r0 .. r0+cnt of the
+// output). Bit j of mask word m <=> row 32m + j matched.
+struct BitmaskSource {
+  const uint32_t* bits;
+  const uint64_t* tile_off;     // exclusive prefix of per-tile counts (tiles of kChunk rows)
+  const uint32_t* start_tile;   // per output item: tile holding rank kChunk*item
+  uint64_t n_words;
+  uint64_t row_offset;
+  __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, EngineSmem& sm, uint32_t* err) const {
+    const int tid = threadIdx.x;
+    const uint64_t t = start_tile[item];
+    uint64_t rank = tile_off[t];  // rank of the first set bit at or after word t*64
+    uint64_t w0 = t * (kChunk / 32);
+    const uint64_t end = r0 + cnt;
+    while (true) {
+      const uint64_t m = w0 + tid;
+      uint32_t word = m < n_words ? __ldg(bits + m) : 0u;
+      uint64_t tot;
+      const uint64_t ex = cta_excl_scan(__popc(word), sm.scan, &tot);
+      uint64_t q = rank + ex;
+      while (word) {
+        const int j = __ffs(word) - 1;
+        word &= word - 1;
+        if (q >= r0 && q < end) sm.vals[q - r0] = row_offset + m * 32 + j;
+        ++q;
+      }
+      rank += tot;
+      w0 += kThreads;
+      if (rank >= end || w0 >= n_words) break;
+    }
+    __syncthreads();
+  }
+};
+
+// Gather through positions (project): rows of the positions column
+// give global positions p; the value is data[p - row_offset].
+struct GatherSource {
+  ColView pos;
+  ColView data;
+  uint64_t row_offset;
+  __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, EngineSmem& sm, uint32_t* err) const {
+    load_rows(pos, r0, cnt, sm);
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      const uint64_t p = sm.vals[i];
+      uint64_t v = 0;
+      if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
+      else v = read_row(data, p - row_offset);
+      sm.vals[i] = v;
+    }
+    __syncthreads();
+  }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(kThreads) engine_kernel(Src src, OutView out, uint32_t* err) {
+  __shared__ EngineSmem sm;
+  const uint64_t n = out.n_dev ? *out.n_dev : out.n;
+  const uint64_t n_items = (n + kChunk - 1) / kChunk;
+  while (true) {
+    if (threadIdx.x == 0) sm.item = atomicAdd(out.ticket, 1u);
+    __syncthreads();
+    const uint32_t item = sm.item;
+    if (item >= n_items) break;
+    const uint64_t r0 = (uint64_t)item * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
+    src.load(item, r0, cnt, sm, err);
+    encode_tile(out, item, r0, cnt, n, sm, err);
+    __syncthreads();
+  }
+}
+
+}  // namespace ms

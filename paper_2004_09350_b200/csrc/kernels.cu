@@ -1,0 +1,500 @@
+// kernels.cu — select / scan / sum / RLE kernels and the launch wrappers.
+#include <atomic>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "launch.h"
+
+namespace ms {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int num_sms() {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
+  }
+  return sms[dev];
+}
+
+template <class K>
+static int persistent_grid(K kernel, int threads, uint64_t items) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t g = (uint64_t)per_sm * num_sms();
+  if (items < g) g = items;
+  return (int)(g ? g : 1);
+}
+
+static uint64_t n_items_hint(const OutView& o) {
+  // an upper bound of the item count for grid sizing (n_dev may be device-resident)
+  return (o.n + kChunk - 1) / kChunk;
+}
+
+// ----------------------------------------------------------------- engine
+cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s) {
+  auto k = engine_kernel<ColSource>;
+  int grid = persistent_grid(k, kThreads, n_items_hint(out));
+  count_launch();
+  k<<<grid, kThreads, 0, s>>>(ColSource{src}, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_engine_bitmask(const uint32_t* bits, const uint64_t* tile_off, const uint32_t* start_tile,
+                                  uint64_t n_words, uint64_t row_offset, const OutView& out, uint32_t* err,
+                                  cudaStream_t s) {
+  auto k = engine_kernel<BitmaskSource>;
+  int grid = persistent_grid(k, kThreads, n_items_hint(out));
+  count_launch();
+  k<<<grid, kThreads, 0, s>>>(BitmaskSource{bits, tile_off, start_tile, n_words, row_offset}, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64_t row_offset, const OutView& out,
+                                 uint32_t* err, cudaStream_t s) {
+  auto k = engine_kernel<GatherSource>;
+  int grid = persistent_grid(k, kThreads, n_items_hint(out));
+  count_launch();
+  k<<<grid, kThreads, 0, s>>>(GatherSource{pos, data, row_offset}, out, err);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- select: predicate
+struct RangePred {
+  uint64_t lo, span;
+  uint32_t neg;
+  __device__ __forceinline__ bool operator()(uint64_t v) const { return ((v - lo) <= span) != (neg != 0); }
+};
+struct BitmapPred {
+  const uint64_t* bm;
+  uint64_t bits;
+  __device__ __forceinline__ bool operator()(uint64_t v) const {
+    return v < bits && ((__ldg(bm + (v >> 6)) >> (v & 63)) & 1ull);
+  }
+};
+
+// Vector-register core of select: per tile of 2048 rows, decode,
+// evaluate the predicate, ballot -> one 32-bit mask word per 32 rows, popc.
+template <class Pred>
+__global__ void __launch_bounds__(kThreads) select_tiles_kernel(ColView c, Pred pred, uint32_t* bits,
+                                                                uint32_t* tile_count, uint32_t* tile_last,
+                                                                uint64_t n_tiles) {
+  __shared__ EngineSmem sm;
+  __shared__ uint32_t wcnt[kThreads / 32], wlast[kThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
+    load_rows(c, r0, cnt, sm);
+    uint32_t cw_ = 0, last = 0;
+    constexpr int kWordsPerWarp = kChunk / 32 / (kThreads / 32);
+#pragma unroll
+    for (int q = 0; q < kWordsPerWarp; ++q) {
+      const uint32_t m = wid * kWordsPerWarp + q;
+      const uint32_t i = m * 32 + lane;
+      const bool p = i < cnt && pred(sm.vals[i]);
+      const uint32_t word = __ballot_sync(kFull, p);
+      if (lane == 0) bits[t * (kChunk / 32) + m] = word;
+      cw_ += __popc(word);
+      if (word) last = m * 32 + 32 - __clz(word);  // 1-based local row of the last match
+    }
+    if (lane == 0) {
+      wcnt[wid] = cw_;
+      wlast[wid] = last;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0, lst = 0;
+      for (int k = 0; k < kThreads / 32; ++k) {
+        tot += wcnt[k];
+        lst = wlast[k] > lst ? wlast[k] : lst;
+      }
+      tile_count[t] = tot;
+      tile_last[t] = lst;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_select_tiles(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* tile_count,
+                                uint32_t* tile_last, uint64_t n_tiles, cudaStream_t s) {
+  if (n_tiles == 0) return cudaSuccess;
+  count_launch();
+  if (p.is_bitmap) {
+    auto k = select_tiles_kernel<BitmapPred>;
+    k<<<persistent_grid(k, kThreads, n_tiles), kThreads, 0, s>>>(c, BitmapPred{p.bitmap, p.bitmap_bits}, bits,
+                                                                 tile_count, tile_last, n_tiles);
+  } else {
+    auto k = select_tiles_kernel<RangePred>;
+    k<<<persistent_grid(k, kThreads, n_tiles), kThreads, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits,
+                                                                 tile_count, tile_last, n_tiles);
+  }
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- generic scan
+// Exclusive prefix over N values in one pass (decoupled look-back); epi(idx,
+// exclusive, value) consumes each entry, epi_total(total) is called once.
+template <class In, class Epi>
+__global__ void __launch_bounds__(kThreads) scan_kernel(In in, Epi epi, uint64_t N, uint64_t* status,
+                                                        uint32_t* ticket) {
+  __shared__ uint64_t scan_sm[16];
+  __shared__ uint32_t s_item;
+  __shared__ uint64_t s_E;
+  const uint64_t n_items = (N + kChunk - 1) / kChunk;
+  const int tid = threadIdx.x;
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= n_items) break;
+    const uint64_t base = (uint64_t)item * kChunk + tid * kVPT;
+    uint64_t v[kVPT];
+    uint64_t tsum = 0;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      v[q] = base + q < N ? in(base + q) : 0;
+      tsum += v[q];
+    }
+    uint64_t tot;
+    const uint64_t ex = cta_excl_scan(tsum, scan_sm, &tot);
+    if (tid < 32) {
+      const uint64_t E = lookback_warp(status, item, tot);
+      if (tid == 0) s_E = E;
+    }
+    __syncthreads();
+    uint64_t off = s_E + ex;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      if (base + q < N) {
+        epi(base + q, off, v[q]);
+        if (base + q == N - 1) epi.total(off + v[q]);
+      }
+      off += v[q];
+    }
+    __syncthreads();
+  }
+}
+
+template <class In, class Epi>
+static cudaError_t run_scan(In in, Epi epi, uint64_t N, uint64_t* status, uint32_t* ticket, cudaStream_t s) {
+  if (N == 0) return cudaSuccess;
+  auto k = scan_kernel<In, Epi>;
+  count_launch();
+  k<<<persistent_grid(k, kThreads, (N + kChunk - 1) / kChunk), kThreads, 0, s>>>(in, epi, N, status, ticket);
+  return cudaGetLastError();
+}
+
+struct U32In {
+  const uint32_t* p;
+  __device__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
+
+// select: tile offsets, output item -> start tile, max position
+struct TileEpi {
+  uint64_t* tile_off;
+  uint32_t* start_tile;
+  const uint32_t* tile_last;
+  unsigned long long* max_pos;
+  uint64_t row_offset;
+  uint64_t T;
+  __device__ void operator()(uint64_t idx, uint64_t off, uint64_t c) const {
+    tile_off[idx] = off;
+    if (c) {
+      for (uint64_t k = (off + kChunk - 1) / kChunk; k * kChunk < off + c; ++k) start_tile[k] = (uint32_t)idx;
+      atomicMax(max_pos, (unsigned long long)(row_offset + idx * kChunk + tile_last[idx] - 1));
+    }
+  }
+  __device__ void total(uint64_t t) const { tile_off[T] = t; }
+};
+
+cudaError_t launch_tile_scan(const uint32_t* tile_count, const uint32_t* tile_last, uint64_t T,
+                             uint64_t row_offset, uint64_t* tile_off, uint32_t* start_tile,
+                             unsigned long long* max_pos, uint64_t* status, uint32_t* ticket, cudaStream_t s) {
+  return run_scan(U32In{tile_count}, TileEpi{tile_off, start_tile, tile_last, max_pos, row_offset, T}, T, status,
+                  ticket, s);
+}
+
+struct CountEpi {
+  uint64_t* off;
+  uint64_t T;
+  __device__ void operator()(uint64_t idx, uint64_t o, uint64_t c) const { off[idx] = o; }
+  __device__ void total(uint64_t t) const { off[T] = t; }
+};
+
+cudaError_t launch_count_scan(const uint32_t* counts, uint64_t T, uint64_t* off, uint64_t* status,
+                              uint32_t* ticket, cudaStream_t s) {
+  return run_scan(U32In{counts}, CountEpi{off, T}, T, status, ticket, s);
+}
+
+// RLE: run starts = exclusive prefix of the lengths; lengths must be >= 1 and
+// sum to n (a corrupt body otherwise)
+struct LenIn {
+  const uint64_t* payload;
+  __device__ uint64_t operator()(uint64_t i) const { return payload[2 * i + 1]; }
+};
+struct StartsEpi {
+  uint64_t* starts;
+  uint64_t R, n;
+  uint32_t* err;
+  __device__ void operator()(uint64_t idx, uint64_t off, uint64_t len) const {
+    starts[idx] = off;
+    if (len == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+  }
+  __device__ void total(uint64_t t) const {
+    starts[R] = t;
+    if (t != n) atomicOr(err, err_bit(MS_E_CORRUPT));
+  }
+};
+
+cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
+                              uint32_t* ticket, uint32_t* err, cudaStream_t s) {
+  return run_scan(LenIn{payload}, StartsEpi{starts, R, n, err}, R, status, ticket, s);
+}
+
+__global__ void chunk_run_kernel(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R; k += stride) {
+    const uint64_t s = starts[k];
+    const uint64_t e = min(starts[k + 1], n);
+    for (uint64_t c = (s + kChunk - 1) / kChunk; c * kChunk < e; ++c) chunk_run[c] = (uint32_t)k;
+  }
+}
+
+cudaError_t launch_chunk_run(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run, cudaStream_t s) {
+  if (R == 0) return cudaSuccess;
+  count_launch();
+  chunk_run_kernel<<<num_sms() * 8, 256, 0, s>>>(starts, R, n, chunk_run);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------ RLE compression
+__global__ void __launch_bounds__(kThreads) rle_count_kernel(const uint64_t* __restrict__ v, uint64_t n,
+                                                             uint32_t* counts) {
+  __shared__ uint32_t wsum[kThreads / 32];
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    uint32_t c = 0;
+    for (uint32_t i = threadIdx.x; i < kChunk; i += kThreads) {
+      const uint64_t r = t * kChunk + i;
+      if (r < n && (r == 0 || v[r] != v[r - 1])) ++c;
+    }
+    c = (uint32_t)warp_sum(c);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t s = 0;
+      for (int k = 0; k < kThreads / 32; ++k) s += wsum[k];
+      counts[t] = s;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_rle_count(const uint64_t* v, uint64_t n, uint32_t* counts, cudaStream_t s) {
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  if (!T) return cudaSuccess;
+  count_launch();
+  rle_count_kernel<<<persistent_grid(rle_count_kernel, kThreads, T), kThreads, 0, s>>>(v, n, counts);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kThreads) rle_write_kernel(const uint64_t* __restrict__ v, uint64_t n,
+                                                             const uint64_t* chunk_off, uint64_t* payload,
+                                                             uint64_t* starts) {
+  __shared__ uint64_t scan_sm[16];
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  const int tid = threadIdx.x;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk + tid * kVPT;
+    uint32_t marks = 0, c = 0;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      const uint64_t r = r0 + q;
+      if (r < n && (r == 0 || v[r] != v[r - 1])) {
+        marks |= 1u << q;
+        ++c;
+      }
+    }
+    uint64_t idx = chunk_off[t] + cta_excl_scan(c, scan_sm, nullptr);
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q)
+      if (marks & (1u << q)) {
+        payload[2 * idx] = v[r0 + q];
+        starts[idx] = r0 + q;
+        ++idx;
+      }
+  }
+}
+
+cudaError_t launch_rle_write(const uint64_t* v, uint64_t n, const uint64_t* chunk_off, uint64_t* payload,
+                             uint64_t* starts, cudaStream_t s) {
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  if (!T) return cudaSuccess;
+  count_launch();
+  rle_write_kernel<<<persistent_grid(rle_write_kernel, kThreads, T), kThreads, 0, s>>>(v, n, chunk_off, payload,
+                                                                                        starts);
+  return cudaGetLastError();
+}
+
+__global__ void rle_len_kernel(const uint64_t* starts, uint64_t R, uint64_t n, uint64_t* payload) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R; k += stride)
+    payload[2 * k + 1] = (k + 1 < R ? starts[k + 1] : n) - starts[k];
+}
+
+cudaError_t launch_rle_len(const uint64_t* starts, uint64_t R, uint64_t n, uint64_t* payload, cudaStream_t s) {
+  if (!R) return cudaSuccess;
+  count_launch();
+  rle_len_kernel<<<num_sms() * 8, 256, 0, s>>>(starts, R, n, payload);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ sums
+// sum of a whole column mod 2^64, using the format identities:
+// RLE sum v*len; FOR B*ref + sum codes; DELTA B*base + sum (B-j) d_j.
+__global__ void __launch_bounds__(kThreads) sum_kernel(ColView c, unsigned long long* out) {
+  __shared__ uint64_t wsum[kThreads / 32];
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  uint64_t acc = 0;
+  switch (c.format) {
+    case MS_UNCOMPR:
+      for (uint64_t i = gtid; i < c.n; i += gthreads) acc += __ldg(c.payload + i);
+      break;
+    case MS_STATIC_BP:
+      for (uint64_t i = gtid; i < c.n; i += gthreads) acc += unpack_at(c.payload, i * c.w, c.w);
+      break;
+    case MS_RLE:
+      for (uint64_t k = gtid; k < c.nruns; k += gthreads) acc += __ldg(c.payload + 2 * k) * __ldg(c.payload + 2 * k + 1);
+      break;
+    default: {
+      const uint64_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
+      for (uint64_t b = gwarp; b < c.nb; b += gwarps) {
+        const uint32_t cw0 = __ldg(c.cw + b);
+        const uint32_t w = __ldg(c.cw + b + 1) - cw0;
+        const uint64_t bit0 = (uint64_t)cw0 * c.B;
+        uint64_t s = 0;
+        if (w) {
+          for (uint32_t j = lane; j < c.B; j += 32) {
+            const uint64_t code = unpack_at(c.payload, bit0 + (uint64_t)j * w, w);
+            s += c.format == MS_DELTA_BP ? (uint64_t)(c.B - j) * code : code;
+          }
+        }
+        if (lane == 0 && c.format != MS_DYN_BP) s += (uint64_t)c.B * __ldg(c.ref + b);
+        acc += s;
+      }
+      for (uint64_t i = gtid; i < c.nrem; i += gthreads) acc += __ldg(c.rem + i);
+      break;
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int k = 0; k < kThreads / 32; ++k) t += wsum[k];
+    if (t) atomicAdd(out, (unsigned long long)t);
+  }
+}
+
+cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err, cudaStream_t s) {
+  count_launch();
+  sum_kernel<<<persistent_grid(sum_kernel, kThreads, ~0ull), kThreads, 0, s>>>(c, out);
+  return cudaGetLastError();
+}
+
+// sum of data at positions (select -> project -> sum fused)
+__global__ void __launch_bounds__(kThreads) sum_at_kernel(ColView data, ColView pos, uint64_t row_offset,
+                                                          unsigned long long* out, uint32_t* err) {
+  __shared__ EngineSmem sm;
+  __shared__ uint64_t wsum[kThreads / 32];
+  const uint64_t T = (pos.n + kChunk - 1) / kChunk;
+  uint64_t acc = 0;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, pos.n - r0);
+    load_rows(pos, r0, cnt, sm);
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      const uint64_t p = sm.vals[i];
+      if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
+      else acc += read_row(data, p - row_offset);
+    }
+    __syncthreads();
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int k = 0; k < kThreads / 32; ++k) t += wsum[k];
+    if (t) atomicAdd(out, (unsigned long long)t);
+  }
+}
+
+cudaError_t launch_sum_at(const ColView& data, const ColView& pos, uint64_t row_offset, unsigned long long* out,
+                          uint32_t* err, cudaStream_t s) {
+  const uint64_t T = (pos.n + kChunk - 1) / kChunk;
+  if (!T) return cudaSuccess;
+  count_launch();
+  sum_at_kernel<<<persistent_grid(sum_at_kernel, kThreads, T), kThreads, 0, s>>>(data, pos, row_offset, out, err);
+  return cudaGetLastError();
+}
+
+// grouped sum with an uncompressed result: per-CTA shared-memory
+// histogram when the groups fit, else global atomics
+constexpr uint32_t kSmemGroups = 1024;
+__global__ void __launch_bounds__(kThreads) sum_grouped_kernel(ColView gid, ColView vals, uint64_t n_groups,
+                                                               unsigned long long* sums, uint32_t* err) {
+  __shared__ EngineSmem sm;
+  __shared__ uint64_t g[kChunk];
+  __shared__ unsigned long long hist[kSmemGroups];
+  const bool use_smem = n_groups <= kSmemGroups;
+  if (use_smem)
+    for (uint32_t k = threadIdx.x; k < n_groups; k += kThreads) hist[k] = 0;
+  const uint64_t T = (gid.n + kChunk - 1) / kChunk;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, gid.n - r0);
+    load_rows(gid, r0, cnt, sm);
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) g[i] = sm.vals[i];
+    __syncthreads();
+    load_rows(vals, r0, cnt, sm);
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      const uint64_t k = g[i];
+      if (k >= n_groups) {
+        atomicOr(err, err_bit(MS_E_RANGE));
+        continue;
+      }
+      if (use_smem) atomicAdd(&hist[k], (unsigned long long)sm.vals[i]);
+      else atomicAdd(&sums[k], (unsigned long long)sm.vals[i]);
+    }
+    __syncthreads();
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < n_groups; k += kThreads)
+      if (hist[k]) atomicAdd(&sums[k], hist[k]);
+  }
+}
+
+cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t n_groups,
+                               unsigned long long* sums, uint32_t* err, cudaStream_t s) {
+  const uint64_t T = (gid.n + kChunk - 1) / kChunk;
+  if (!T) return cudaSuccess;
+  count_launch();
+  sum_grouped_kernel<<<persistent_grid(sum_grouped_kernel, kThreads, T), kThreads, 0, s>>>(gid, vals, n_groups,
+                                                                                          sums, err);
+  return cudaGetLastError();
+}
+
+}  // namespace ms

@@ -1,0 +1,59 @@
+// launch.h — host-side launch wrappers of libms' kernels (internal, C++).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ms.h"
+
+namespace ms {
+
+struct ColView;
+struct OutView;
+
+// instrumentation: kernel launches issued by this library
+void count_launch();
+uint64_t launch_count();
+
+// predicate in the range form keep = ((v - lo) <= span) != neg, or a bitmap
+struct PredSpec {
+  int is_bitmap;
+  uint64_t lo, span;
+  uint32_t neg;
+  const uint64_t* bitmap;
+  uint64_t bitmap_bits;
+};
+
+cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s);
+cudaError_t launch_engine_bitmask(const uint32_t* bits, const uint64_t* tile_off, const uint32_t* start_tile,
+                                  uint64_t n_words, uint64_t row_offset, const OutView& out, uint32_t* err,
+                                  cudaStream_t s);
+cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64_t row_offset, const OutView& out,
+                                 uint32_t* err, cudaStream_t s);
+
+cudaError_t launch_select_tiles(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* tile_count,
+                                uint32_t* tile_last, uint64_t n_tiles, cudaStream_t s);
+// exclusive scan of per-tile counts -> tile_off[0..T], start_tile[], max position
+cudaError_t launch_tile_scan(const uint32_t* tile_count, const uint32_t* tile_last, uint64_t T,
+                             uint64_t row_offset, uint64_t* tile_off, uint32_t* start_tile,
+                             unsigned long long* max_pos, uint64_t* status, uint32_t* ticket, cudaStream_t s);
+// RLE run starts (exclusive prefix of lengths), validation against n
+cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
+                              uint32_t* ticket, uint32_t* err, cudaStream_t s);
+cudaError_t launch_chunk_run(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run, cudaStream_t s);
+// RLE compression of raw device values
+cudaError_t launch_rle_count(const uint64_t* v, uint64_t n, uint32_t* counts, cudaStream_t s);
+cudaError_t launch_count_scan(const uint32_t* counts, uint64_t T, uint64_t* off, uint64_t* status,
+                              uint32_t* ticket, cudaStream_t s);
+cudaError_t launch_rle_write(const uint64_t* v, uint64_t n, const uint64_t* chunk_off, uint64_t* payload,
+                             uint64_t* starts, cudaStream_t s);
+cudaError_t launch_rle_len(const uint64_t* starts, uint64_t R, uint64_t n, uint64_t* payload, cudaStream_t s);
+
+cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err, cudaStream_t s);
+cudaError_t launch_sum_at(const ColView& data, const ColView& pos, uint64_t row_offset, unsigned long long* out,
+                          uint32_t* err, cudaStream_t s);
+cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t n_groups,
+                               unsigned long long* sums, uint32_t* err, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace ms

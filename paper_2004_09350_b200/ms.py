@@ -1,0 +1,330 @@
+"""Python binding of libms (include/ms.h): argument marshalling only.
+
+Every step of every operator runs in libms.so's sm_100a kernels; this module
+converts arguments, supplies PyTorch's caching allocator and current CUDA
+stream to the library, and owns the returned columns. There is no CPU or
+PyTorch fallback: if libms.so is missing, importing this module fails.
+
+Names follow the C ABI (ms_compress -> compress, ...). Citations: PAPER.md
+P:n, SPEC.md S:n (see include/ms.h for the per-function contract).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import NamedTuple, Optional
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libms.so")
+
+UNCOMPR, STATIC_BP, DYN_BP, DELTA_BP, FOR_BP, RLE = range(6)
+FORMAT_NAMES = ("UNCOMPR", "STATIC_BP", "DYN_BP", "DELTA_BP", "FOR_BP", "RLE")
+EQ, NE, LT, LE, GT, GE, BETWEEN, IN_BITMAP = range(8)
+OP_NAMES = ("EQ", "NE", "LT", "LE", "GT", "GE", "BETWEEN", "IN_BITMAP")
+STATUS = ("MS_OK", "MS_E_INVALID", "MS_E_WIDTH_OVERFLOW", "MS_E_UNSUPPORTED", "MS_E_RANGE", "MS_E_CORRUPT",
+          "MS_E_NOMEM", "MS_E_CUDA")
+FLAG_SHRINK = 1
+
+
+class MsError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {STATUS[code] if 0 <= code < len(STATUS) else code}")
+        self.code = code
+
+
+class Fmt(NamedTuple):
+    """Column descriptor {format, bit width, block size} (ms_fmt)."""
+    format: int
+    bit_width: int = 0
+    block_size: int = 0
+
+    def __str__(self):
+        name = FORMAT_NAMES[self.format]
+        if self.format == STATIC_BP:
+            return f"{name}{{{self.bit_width or 'auto'}}}"
+        if self.format in (DYN_BP, DELTA_BP, FOR_BP):
+            return f"{name}{{{self.block_size}}}"
+        return name
+
+
+def uncompr() -> Fmt: return Fmt(UNCOMPR)
+def static_bp(w: int = 0) -> Fmt: return Fmt(STATIC_BP, w, 0)
+def dyn_bp(B: int = 512) -> Fmt: return Fmt(DYN_BP, 0, B)
+def delta_bp(B: int = 512) -> Fmt: return Fmt(DELTA_BP, 0, B)
+def for_bp(B: int = 512) -> Fmt: return Fmt(FOR_BP, 0, B)
+def rle() -> Fmt: return Fmt(RLE)
+
+
+class _Fmt(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("bit_width", ctypes.c_uint32), ("block_size", ctypes.c_uint32),
+                ("_reserved", ctypes.c_uint32)]
+
+
+class _Column(ctypes.Structure):
+    _fields_ = [("fmt", _Fmt), ("n", ctypes.c_uint64), ("n_blocks", ctypes.c_uint64), ("n_rem", ctypes.c_uint64),
+                ("n_runs", ctypes.c_uint64), ("payload_words", ctypes.c_uint64), ("payload", ctypes.c_void_p),
+                ("cw", ctypes.c_void_p), ("ref", ctypes.c_void_p), ("rem", ctypes.c_void_p),
+                ("alloc", ctypes.c_void_p), ("alloc_bytes", ctypes.c_uint64)]
+
+
+class _Pred(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("_reserved", ctypes.c_uint32), ("a", ctypes.c_uint64),
+                ("b", ctypes.c_uint64), ("bitmap", ctypes.c_void_p), ("bitmap_bits", ctypes.c_uint64)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class _Ctx(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_void_p), ("alloc", _ALLOC_FN), ("free", _FREE_FN), ("alloc_ctx", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32), ("_reserved", ctypes.c_uint32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libms.so not built ({LIB_PATH}); run `python build_native.py libms` — "
+                          "there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    C, st, vp, u64 = P(_Column), ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64
+    sig = {
+        "ms_compress": ([P(_Ctx), vp, u64, _Fmt, C], st),
+        "ms_decompress": ([P(_Ctx), C, vp], st),
+        "ms_morph": ([P(_Ctx), C, _Fmt, C], st),
+        "ms_select": ([P(_Ctx), C, P(_Pred), u64, _Fmt, C], st),
+        "ms_project": ([P(_Ctx), C, C, u64, _Fmt, C], st),
+        "ms_agg_sum": ([P(_Ctx), C, C, u64, vp], st),
+        "ms_agg_sum_grouped": ([P(_Ctx), C, C, u64, vp], st),
+        "ms_column_to_device": ([P(_Ctx), C, C], st),
+        "ms_column_to_host": ([P(_Ctx), C, C], st),
+        "ms_check_errors": ([P(_Ctx)], st),
+        "ms_column_release": ([P(_Ctx), C], None),
+        "ms_column_bytes": ([C], u64),
+        "ms_status_str": ([ctypes.c_int], ctypes.c_char_p),
+        "ms_abi_version": ([], ctypes.c_int),
+        "ms_launch_count": ([], u64),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+# ------------------------------------------------------------ allocator
+_live = {}
+
+
+@_ALLOC_FN
+def _torch_alloc(_ctx, size, stream):
+    try:
+        ptr = torch.cuda.caching_allocator_alloc(int(size), torch.cuda.current_device(), int(stream or 0))
+        return ptr
+    except Exception:  # out of memory -> NULL -> MS_E_NOMEM
+        return None
+
+
+@_FREE_FN
+def _torch_free(_ctx, ptr, _stream):
+    if ptr:
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+
+def _ctx(stream: Optional[torch.cuda.Stream] = None, flags: int = 0) -> _Ctx:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return _Ctx(stream=stream.cuda_stream, alloc=_torch_alloc, free=_torch_free, alloc_ctx=None, flags=flags)
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise MsError(rc, where)
+
+
+def _ptr(t) -> int:
+    if isinstance(t, torch.Tensor):
+        if not t.is_cuda:
+            raise ValueError("device tensor expected")
+        if not t.is_contiguous():
+            raise ValueError("contiguous tensor expected")
+        return t.data_ptr()
+    return int(t)
+
+
+class Column:
+    """A device column owned by Python (released through ms_column_release)."""
+
+    def __init__(self, c: _Column, owned: bool = True):
+        self._c = c
+        self._owned = owned
+
+    def __del__(self):
+        try:
+            if self._owned and self._c.alloc:
+                _lib.ms_column_release(ctypes.byref(_ctx()), ctypes.byref(self._c))
+        except Exception:
+            pass
+
+    @property
+    def fmt(self) -> Fmt:
+        f = self._c.fmt
+        return Fmt(f.format, f.bit_width, f.block_size)
+
+    n = property(lambda self: int(self._c.n))
+    n_blocks = property(lambda self: int(self._c.n_blocks))
+    n_rem = property(lambda self: int(self._c.n_rem))
+    n_runs = property(lambda self: int(self._c.n_runs))
+    payload_words = property(lambda self: int(self._c.payload_words))
+
+    def footprint(self) -> int:
+        """image bytes: payload + cw + ref + rem (ms_column_bytes)"""
+        return int(_lib.ms_column_bytes(ctypes.byref(self._c)))
+
+    def images(self) -> dict:
+        """Copy the four image sections to host numpy arrays (ms_column_to_host)."""
+        c = self._c
+        blockf = c.fmt.format in (DYN_BP, DELTA_BP, FOR_BP)
+        out = {
+            "payload": np.zeros(c.payload_words, np.uint64),
+            "cw": np.zeros(c.n_blocks + 1 if blockf else 0, np.uint32),
+            "ref": np.zeros(c.n_blocks if c.fmt.format in (DELTA_BP, FOR_BP) else 0, np.uint64),
+            "rem": np.zeros(c.n_rem if blockf else 0, np.uint64),
+        }
+        h = _Column()
+        for k in ("payload", "cw", "ref", "rem"):
+            setattr(h, k, out[k].ctypes.data if out[k].size else None)
+        _check(_lib.ms_column_to_host(ctypes.byref(_ctx()), ctypes.byref(c), ctypes.byref(h)), "ms_column_to_host")
+        return out
+
+    @staticmethod
+    def from_host(fmt: Fmt, n: int, payload, cw=None, ref=None, rem=None, n_runs: int = 0) -> "Column":
+        """Upload host image sections into a new device column (ms_column_to_device)."""
+        h = _Column()
+        h.fmt = _Fmt(fmt.format, fmt.bit_width, fmt.block_size, 0)
+        h.n = n
+        keep = []
+
+        def arr(x, dt):
+            a = np.ascontiguousarray(np.asarray(x if x is not None else [], dtype=dt))
+            keep.append(a)
+            return a
+
+        p = arr(payload, np.uint64)
+        h.payload = p.ctypes.data if p.size else None
+        h.payload_words = p.size
+        if fmt.format in (DYN_BP, DELTA_BP, FOR_BP):
+            B = fmt.block_size
+            h.n_blocks, h.n_rem = n // B, n % B
+            a = arr(cw, np.uint32); h.cw = a.ctypes.data
+            a = arr(ref, np.uint64); h.ref = a.ctypes.data if a.size else None
+            a = arr(rem, np.uint64); h.rem = a.ctypes.data if a.size else None
+        h.n_runs = n_runs
+        out = _Column()
+        _check(_lib.ms_column_to_device(ctypes.byref(_ctx()), ctypes.byref(h), ctypes.byref(out)),
+               "ms_column_to_device")
+        torch.cuda.current_stream().synchronize()  # host arrays may be pageable / freed after return
+        return Column(out)
+
+    def __repr__(self):
+        return f"Column({self.fmt}, n={self.n}, bytes={self.footprint()})"
+
+
+def _fmt(f) -> _Fmt:
+    f = Fmt(*f) if not isinstance(f, Fmt) else f
+    return _Fmt(f.format, f.bit_width, f.block_size, 0)
+
+
+def compress(values, fmt, n: Optional[int] = None, stream=None, flags: int = 0) -> Column:
+    """ms_compress: values = CUDA tensor of 64-bit integers (uint64 bit patterns) or a device pointer."""
+    if n is None:
+        n = values.numel()
+    out = _Column()
+    _check(_lib.ms_compress(ctypes.byref(_ctx(stream, flags)), _ptr(values) if n else None, n, _fmt(fmt),
+                            ctypes.byref(out)), "ms_compress")
+    return Column(out)
+
+
+def decompress(col: Column, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """ms_decompress into a torch.int64 CUDA tensor (uint64 bit patterns)."""
+    if out is None:
+        out = torch.empty(col.n, dtype=torch.int64, device="cuda")
+    _check(_lib.ms_decompress(ctypes.byref(_ctx(stream)), ctypes.byref(col._c), _ptr(out) if col.n else None),
+           "ms_decompress")
+    return out
+
+
+def morph(col: Column, fmt, stream=None, flags: int = 0) -> Column:
+    out = _Column()
+    _check(_lib.ms_morph(ctypes.byref(_ctx(stream, flags)), ctypes.byref(col._c), _fmt(fmt), ctypes.byref(out)),
+           "ms_morph")
+    return Column(out)
+
+
+def select(col: Column, op: int, a: int = 0, b: int = 0, bitmap: Optional[torch.Tensor] = None,
+           bitmap_bits: int = 0, row_offset: int = 0, out_fmt=None, stream=None, flags: int = 0) -> Column:
+    if out_fmt is None:
+        out_fmt = delta_bp(512)
+    p = _Pred(op=op, a=a & (2**64 - 1), b=b & (2**64 - 1), bitmap=_ptr(bitmap) if bitmap is not None else None,
+              bitmap_bits=bitmap_bits)
+    out = _Column()
+    _check(_lib.ms_select(ctypes.byref(_ctx(stream, flags)), ctypes.byref(col._c), ctypes.byref(p), row_offset,
+                          _fmt(out_fmt), ctypes.byref(out)), "ms_select")
+    return Column(out)
+
+
+def project(data: Column, positions: Column, row_offset: int = 0, out_fmt=None, stream=None,
+            flags: int = 0) -> Column:
+    if out_fmt is None:
+        out_fmt = uncompr()
+    out = _Column()
+    _check(_lib.ms_project(ctypes.byref(_ctx(stream, flags)), ctypes.byref(data._c), ctypes.byref(positions._c),
+                           row_offset, _fmt(out_fmt), ctypes.byref(out)), "ms_project")
+    return Column(out)
+
+
+def agg_sum(col: Column, positions: Optional[Column] = None, row_offset: int = 0,
+            out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """ms_agg_sum -> 1-element torch.int64 CUDA tensor holding the uint64 sum bits (no sync)."""
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64, device="cuda")
+    _check(_lib.ms_agg_sum(ctypes.byref(_ctx(stream)), ctypes.byref(col._c),
+                           ctypes.byref(positions._c) if positions is not None else None, row_offset, _ptr(out)),
+           "ms_agg_sum")
+    return out
+
+
+def agg_sum_grouped(gid: Column, vals: Column, n_groups: int, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(n_groups, dtype=torch.int64, device="cuda")
+    _check(_lib.ms_agg_sum_grouped(ctypes.byref(_ctx(stream)), ctypes.byref(gid._c), ctypes.byref(vals._c),
+                                   n_groups, _ptr(out) if n_groups else None), "ms_agg_sum_grouped")
+    return out
+
+
+def check_errors(stream=None):
+    _check(_lib.ms_check_errors(ctypes.byref(_ctx(stream))), "ms_check_errors")
+
+
+def launch_count() -> int:
+    return int(_lib.ms_launch_count())
+
+
+def u64(t: torch.Tensor) -> int:
+    """uint64 value of a 1-element int64 tensor (bit pattern)."""
+    return int(t.item()) & (2**64 - 1)
+
+
+def to_u64_numpy(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)

@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact
+on every image section, on seeded inputs spanning several 2048-row tiles, a
+ragged tail and the edge cases (empty, one value, block +-1, all-zero, 64-bit
+values, wrap-around deltas)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.gpu_util import (assert_same_image, get_ms, oracle_fmt, oracle_op, rand_values, to_torch)
+
+pytestmark = pytest.mark.gpu
+
+LENGTHS = [0, 1, 127, 128, 129, 2047, 2048, 2049, 3 * 2048 + 7, 70_001]
+KINDS = ["small", "wide", "sorted", "runs", "outlier", "zeros"]
+
+
+def all_fmts():
+    ms = get_ms()
+    f = [ms.uncompr(), ms.static_bp(0), ms.static_bp(64), ms.rle()]
+    for B in (128, 256, 512, 1024, 2048):
+        f += [ms.dyn_bp(B), ms.for_bp(B), ms.delta_bp(B)]
+    return f
+
+
+@pytest.fixture(scope="module")
+def rng():
+    return np.random.default_rng(2024)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_compress_decompress(kind, rng):
+    ms = get_ms()
+    for n in LENGTHS:
+        v = rand_values(n, kind, rng)
+        t = to_torch(v)
+        for f in all_fmts():
+            oc = O.encode(v, *oracle_fmt(f))
+            gc = ms.compress(t, f)
+            assert_same_image(gc, oc, f"compress {f} {kind} n={n}")
+            back = ms.to_u64_numpy(ms.decompress(gc)) if n else np.zeros(0, np.uint64)
+            assert np.array_equal(back, v), f"decompress {f} {kind} n={n}"
+
+
+def test_static_explicit_widths(rng):
+    ms = get_ms()
+    for w in (1, 3, 7, 10, 13, 20, 31, 32, 33, 40, 63):
+        v = rng.integers(0, 1 << w, 5000, dtype=np.uint64)
+        gc = ms.compress(to_torch(v), ms.static_bp(w))
+        assert_same_image(gc, O.encode(v, O.STATIC_BP, w), f"static w={w}")
+        assert np.array_equal(ms.to_u64_numpy(ms.decompress(gc)), v)
+
+
+def test_width_overflow(rng):
+    ms = get_ms()
+    v = np.array([1, 2, 1 << 12], np.uint64)
+    with pytest.raises(ms.MsError) as e:
+        ms.compress(to_torch(v), ms.static_bp(8))
+    assert e.value.code == 2  # MS_E_WIDTH_OVERFLOW
+
+
+def test_invalid_descriptors():
+    ms = get_ms()
+    with pytest.raises(ms.MsError):
+        ms.compress(to_torch(np.arange(10, dtype=np.uint64)), ms.Fmt(ms.DYN_BP, 0, 100))
+    with pytest.raises(ms.MsError):
+        ms.compress(to_torch(np.arange(10, dtype=np.uint64)), ms.Fmt(9, 0, 0))
+
+
+@pytest.mark.parametrize("kind", ["small", "sorted", "runs", "outlier"])
+def test_morph_pairs(kind, rng):
+    ms = get_ms()
+    fm = [ms.uncompr(), ms.static_bp(0), ms.dyn_bp(512), ms.for_bp(256), ms.delta_bp(2048), ms.delta_bp(128),
+          ms.rle()]
+    for n in (0, 2049, 3 * 2048 + 7, 50_000):
+        v = rand_values(n, kind, rng)
+        t = to_torch(v)
+        for a in fm:
+            ga = ms.compress(t, a)
+            oa = O.encode(v, *oracle_fmt(a))
+            for b in fm:
+                gm = ms.morph(ga, b)
+                assert_same_image(gm, O.morph(oa, *oracle_fmt(b)), f"morph {a}->{b} {kind} n={n}")
+
+
+PREDS = None
+
+
+def preds(v):
+    ms = get_ms()
+    lo = int(np.sort(v)[len(v) // 3]) if len(v) else 5
+    return [(ms.EQ, lo, 0), (ms.NE, lo, 0), (ms.LT, lo, 0), (ms.LE, lo, 0), (ms.GT, lo, 0), (ms.GE, lo, 0),
+            (ms.BETWEEN, lo, lo + 40), (ms.LT, 0, 0), (ms.GE, 0, 0), (ms.GT, 2**64 - 1, 0),
+            (ms.EQ, 2**64 - 1, 0)]
+
+
+@pytest.mark.parametrize("kind", ["small", "sorted", "runs", "outlier", "wide"])
+def test_select(kind, rng):
+    ms = get_ms()
+    in_fmts = [ms.uncompr(), ms.static_bp(0), ms.dyn_bp(512), ms.for_bp(128), ms.delta_bp(2048), ms.rle()]
+    out_fmts = [ms.delta_bp(512), ms.uncompr(), ms.for_bp(128), ms.dyn_bp(2048), ms.static_bp(0),
+                ms.static_bp(40), ms.rle(), ms.delta_bp(128)]
+    for n in (1, 2049, 3 * 2048 + 7, 100_003):
+        v = rand_values(n, kind, rng)
+        t = to_torch(v)
+        for fi in in_fmts:
+            gi = ms.compress(t, fi)
+            oi = O.encode(v, *oracle_fmt(fi))
+            for op, a, b in preds(v):
+                for fo in out_fmts:
+                    for off in (0, 5_000_000_000):
+                        gs = ms.select(gi, op, a, b, row_offset=off, out_fmt=fo)
+                        os_ = O.select(oi, oracle_op(op), a, b, row_offset=off, out_fmt=oracle_fmt(fo)[0],
+                                       out_width=fo.bit_width, out_block=fo.block_size)
+                        assert_same_image(gs, os_, f"select {fi} {op} {a} -> {fo} {kind} n={n} off={off}")
+
+
+def test_select_bitmap(rng):
+    ms = get_ms()
+    import torch
+    bits = 200_000
+    words = rng.integers(0, 2**64 - 1, (bits + 63) // 64, dtype=np.uint64, endpoint=True)
+    words &= rng.integers(0, 2**64 - 1, words.size, dtype=np.uint64, endpoint=True)  # ~25% set
+    bm = to_torch(words)
+    v = rng.integers(0, 210_000, 70_000).astype(np.uint64)
+    for fi in (ms.static_bp(18), ms.uncompr(), ms.dyn_bp(512)):
+        gi = ms.compress(to_torch(v), fi)
+        oi = O.encode(v, *oracle_fmt(fi))
+        gs = ms.select(gi, ms.IN_BITMAP, bitmap=bm, bitmap_bits=bits, out_fmt=ms.delta_bp(512))
+        os_ = O.select(oi, O.IN_BITMAP, bitmap=words, bitmap_bits=bits, out_fmt=O.DELTA_BP, out_block=512)
+        assert_same_image(gs, os_, f"bitmap select {fi}")
+
+
+@pytest.mark.parametrize("kind", ["small", "wide", "sorted", "runs"])
+def test_project(kind, rng):
+    ms = get_ms()
+    n = 3 * 2048 + 77
+    v = rand_values(n, kind, rng)
+    t = to_torch(v)
+    off = 1000
+    sorted_pos = np.sort(rng.choice(n, 2500, replace=False)).astype(np.uint64) + np.uint64(off)
+    unsorted_pos = rng.integers(0, n, 3000).astype(np.uint64) + np.uint64(off)
+    data_fmts = [ms.uncompr(), ms.static_bp(0), ms.dyn_bp(512), ms.for_bp(512), ms.delta_bp(128), ms.rle()]
+    pos_fmts = [ms.delta_bp(512), ms.uncompr(), ms.static_bp(0), ms.rle()]
+    out_fmts = [ms.for_bp(512), ms.uncompr(), ms.dyn_bp(128), ms.static_bp(0), ms.delta_bp(512)]
+    for fd in data_fmts:
+        gd = ms.compress(t, fd)
+        od = O.encode(v, *oracle_fmt(fd))
+        for pos in (sorted_pos, unsorted_pos):
+            for fp in pos_fmts:
+                if fp.format == ms.RLE and pos is unsorted_pos:
+                    continue
+                gp = ms.compress(to_torch(pos), fp)
+                op_ = O.encode(pos, *oracle_fmt(fp))
+                for fo in out_fmts:
+                    gr = ms.project(gd, gp, off, fo)
+                    orr = O.project(od, op_, off, *oracle_fmt(fo))
+                    assert_same_image(gr, orr, f"project {fd} @ {fp} -> {fo} {kind}")
+
+
+def test_project_range_error(rng):
+    ms = get_ms()
+    d = ms.compress(to_torch(np.arange(100, dtype=np.uint64)), ms.for_bp(128))
+    p = ms.compress(to_torch(np.array([5, 100], np.uint64)), ms.uncompr())
+    with pytest.raises(ms.MsError) as e:
+        ms.project(d, p, 0, ms.uncompr())
+    assert e.value.code == 4  # MS_E_RANGE
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_agg_sum(kind, rng):
+    ms = get_ms()
+    for n in (0, 1, 2049, 3 * 512 + 11, 100_001):
+        v = rand_values(n, kind, rng)
+        t = to_torch(v)
+        expect = O.agg_sum(O.encode(v, O.UNCOMPR))
+        for f in all_fmts():
+            g = ms.compress(t, f)
+            assert ms.u64(ms.agg_sum(g)) == expect, f"sum {f} {kind} n={n}"
+        if n:
+            pos = np.sort(rng.choice(n, max(1, n // 3), replace=False)).astype(np.uint64) + np.uint64(7)
+            ep = O.agg_sum(O.encode(v, O.UNCOMPR), O.encode(pos, O.UNCOMPR), 7)
+            for fd in (ms.for_bp(512), ms.static_bp(0), ms.delta_bp(512), ms.rle(), ms.dyn_bp(128)):
+                for fp in (ms.delta_bp(512), ms.uncompr(), ms.rle()):
+                    g = ms.agg_sum(ms.compress(t, fd), ms.compress(to_torch(pos), fp), 7)
+                    assert ms.u64(g) == ep, f"sum_at {fd} {fp} {kind} n={n}"
+    ms.check_errors()
+
+
+def test_agg_sum_grouped(rng):
+    ms = get_ms()
+    for n_groups in (7, 1000, 5000):
+        n = 50_000
+        g = rng.integers(0, n_groups, n).astype(np.uint64)
+        v = rand_values(n, "wide", rng)
+        expect = O.agg_sum_grouped(O.encode(g, O.UNCOMPR), O.encode(v, O.UNCOMPR), n_groups)
+        for fg in (ms.uncompr(), ms.static_bp(0), ms.dyn_bp(512)):
+            for fv in (ms.dyn_bp(512), ms.uncompr(), ms.for_bp(128)):
+                out = ms.agg_sum_grouped(ms.compress(to_torch(g), fg), ms.compress(to_torch(v), fv), n_groups)
+                assert np.array_equal(ms.to_u64_numpy(out), expect), (n_groups, fg, fv)
+    ms.check_errors()
+    bad = ms.compress(to_torch(np.array([1, 2, 9], np.uint64)), ms.uncompr())
+    vals = ms.compress(to_torch(np.array([1, 2, 3], np.uint64)), ms.uncompr())
+    ms.agg_sum_grouped(bad, vals, 5)
+    with pytest.raises(ms.MsError) as e:
+        ms.check_errors()
+    assert e.value.code == 4
+
+
+def test_host_roundtrip(rng):
+    ms = get_ms()
+    v = rand_values(10_000, "outlier", rng)
+    oc = O.encode(v, O.FOR_BP, 0, 512)
+    g = ms.Column.from_host(ms.for_bp(512), oc.n, oc.payload, oc.cw, oc.ref, oc.rem)
+    assert_same_image(g, oc, "from_host")
+    assert np.array_equal(ms.to_u64_numpy(ms.decompress(g)), v)
