@@ -203,6 +203,19 @@ MS_API int ms_abi_version(void);
  * for bench.py's gpu_launches) */
 MS_API uint64_t ms_launch_count(void);
 
+/* Kernel timing instrumentation: when enabled, every kernel launch is
+ * bracketed by CUDA events recorded on its launching stream. ms_profile_read
+ * waits for the recorded events, writes up to max per-kernel aggregates
+ * (name, launches, summed milliseconds) into out (host), clears the records
+ * and returns the number of distinct kernels. */
+typedef struct {
+  char name[48];
+  uint64_t launches;
+  double total_ms;
+} ms_kernel_time;
+MS_API void ms_profile_enable(int on);
+MS_API int ms_profile_read(ms_kernel_time *out, int max);
+
 #ifdef __cplusplus
 }
 #endif

@@ -425,6 +425,8 @@ extern "C" {
 
 int ms_abi_version(void) { return MS_ABI_VERSION; }
 uint64_t ms_launch_count(void) { return launch_count(); }
+void ms_profile_enable(int on) { profile_enable(on); }
+int ms_profile_read(ms_kernel_time* out, int max) { return profile_read(out, max); }
 
 const char* ms_status_str(ms_status s) {
   switch (s) {
@@ -561,18 +563,18 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   MS_TRY(make_pred(pred, ps));
   Ctx ctx(ctx_);
   const uint64_t n = in->n;
-  const uint64_t T = (n + kChunk - 1) / kChunk;
-  const uint64_t n_words = T * (kChunk / 32);
+  const uint64_t NS = (n + kSegRows - 1) / kSegRows;  // 512-row segments
+  const uint64_t n_words = NS * kSegWords;
+  const uint64_t items_max = (n + kChunk - 1) / kChunk + 1;
   Scratch sc(ctx);
-  const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] max position
+  const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] 1 + max position
   const uint64_t o_bits = sc.add(4 * n_words, false);
-  const uint64_t o_cnt = sc.add(4 * (T + 1), false);
-  const uint64_t o_last = sc.add(4 * (T + 1), false);
-  const uint64_t o_off = sc.add(8 * (T + 1), true);
-  const uint64_t o_start = sc.add(4 * (T + 1), false);
-  const uint64_t o_st1 = sc.add(8 * ((T + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_seg = sc.add(4 * (NS + 1), false);
+  const uint64_t o_off = sc.add(8 * (NS + 1), true);
+  const uint64_t o_start = sc.add(4 * (items_max + 1), false);
+  const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
   const uint64_t o_tk1 = sc.add(8, true);
-  const uint64_t o_st2 = sc.add(8 * (T + 1), true);
+  const uint64_t o_st2 = sc.add(8 * (items_max + 1), true);
   const uint64_t o_tk2 = sc.add(8, true);
   RlePrep rp;
   plan_rle(sc, in, rp);
@@ -580,18 +582,17 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   uint32_t* err = sc.at<uint32_t>(o_meta);
   ColView src = view_of(in);
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
-  uint64_t* tile_off = sc.at<uint64_t>(o_off);
-  MS_TRY_CUDA(launch_select_tiles(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_cnt), sc.at<uint32_t>(o_last),
-                                  T, ctx.s));
-  MS_TRY_CUDA(launch_tile_scan(sc.at<uint32_t>(o_cnt), sc.at<uint32_t>(o_last), T, row_offset, tile_off,
-                               sc.at<uint32_t>(o_start), sc.at<unsigned long long>(o_meta + 8),
-                               sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1), ctx.s));
+  uint64_t* seg_off = sc.at<uint64_t>(o_off);
+  MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, ctx.s));
+  MS_TRY_CUDA(launch_seg_scan(sc.at<uint32_t>(o_seg), NS, row_offset, seg_off, sc.at<uint32_t>(o_start),
+                              sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1),
+                              ctx.s));
   uint64_t h[3] = {0, 0, 0};
-  if (T) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], tile_off + T, 8, cudaMemcpyDeviceToHost, ctx.s));
+  if (NS) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], seg_off + NS, 8, cudaMemcpyDeviceToHost, ctx.s));
   MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
   MS_TRY(status_from_bits((uint32_t)h[0]));
-  const uint64_t n_out = T ? h[2] : 0;
-  const uint64_t max_pos = h[1];
+  const uint64_t n_out = NS ? h[2] : 0;
+  const uint64_t max_pos = h[1] ? h[1] - 1 : 0;
   // size the output (n_out and the largest position are known now)
   uint64_t cap = 0;
   ms_fmt f = out_fmt;
@@ -625,7 +626,7 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   if (f.format == MS_UNCOMPR || f.format == MS_RLE || f.format == MS_STATIC_BP) out->payload_words = cap;
   if (n_out) {
     OutView ov = out_view(out, sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2));
-    cudaError_t e = launch_engine_bitmask(sc.at<uint32_t>(o_bits), tile_off, sc.at<uint32_t>(o_start), n_words,
+    cudaError_t e = launch_engine_bitmask(sc.at<uint32_t>(o_bits), seg_off, sc.at<uint32_t>(o_start), n_words,
                                           row_offset, ov, err, ctx.s);
     if (e != cudaSuccess) {
       release(ctx, out);

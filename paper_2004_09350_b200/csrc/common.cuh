@@ -23,6 +23,8 @@ constexpr int kChunk = 2048;               // rows per work item / tile
 constexpr int kThreads = 256;              // CTA size of the generic engine
 constexpr int kVPT = kChunk / kThreads;    // 8 values per thread
 constexpr int kMaxBlocksPerChunk = kChunk / 128;
+constexpr int kSegRows = 512;             // rows per select segment (16 mask words)
+constexpr int kSegWords = kSegRows / 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 // device error bits: bit s <=> ms_status s

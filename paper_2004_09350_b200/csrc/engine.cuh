@@ -168,15 +168,15 @@ struct ColSource {
 // output). Bit j of mask word m <=> row 32m + j matched.
 struct BitmaskSource {
   const uint32_t* bits;
-  const uint64_t* tile_off;     // exclusive prefix of per-tile counts (tiles of kChunk rows)
-  const uint32_t* start_tile;   // per output item: tile holding rank kChunk*item
+  const uint64_t* seg_off;      // exclusive prefix of per-segment counts (segments of kSegRows rows)
+  const uint32_t* start_seg;    // per output item: segment holding rank kChunk*item
   uint64_t n_words;
   uint64_t row_offset;
   __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, EngineSmem& sm, uint32_t* err) const {
     const int tid = threadIdx.x;
-    const uint64_t t = start_tile[item];
-    uint64_t rank = tile_off[t];  // rank of the first set bit at or after word t*64
-    uint64_t w0 = t * (kChunk / 32);
+    const uint64_t t = start_seg[item];
+    uint64_t rank = seg_off[t];  // rank of the first set bit at or after word t*kSegWords
+    uint64_t w0 = t * kSegWords;
     const uint64_t end = r0 + cnt;
     while (true) {
       const uint64_t m = w0 + tid;

@@ -1,8 +1,12 @@
 // kernels.cu — select / scan / sum / RLE kernels and the launch wrappers.
 #include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "engine.cuh"
+#include "select_fast.cuh"
 #include "launch.h"
 
 namespace ms {
@@ -10,6 +14,78 @@ namespace ms {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+// ---------------------------------------------------------- profiling
+// Optional CUDA-event timing of every kernel launch, on the launching stream
+// (bench.py reads the dominant kernel's average duration from here).
+namespace {
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<int> g_prof_on{0};
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(const char* name, cudaStream_t s) : name_(name), s_(s), on_(g_prof_on.load() != 0) {
+  count_launch();
+  if (!on_) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  a_ = (void*)prof_event();
+  b_ = (void*)prof_event();
+  cudaEventRecord((cudaEvent_t)a_, s_);
+}
+ProfScope::~ProfScope() {
+  if (!on_) return;
+  cudaEventRecord((cudaEvent_t)b_, s_);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_recs.push_back({name_, (cudaEvent_t)a_, (cudaEvent_t)b_});
+}
+
+void profile_enable(int on) { g_prof_on.store(on); }
+
+int profile_read(ms_kernel_time* out, int max) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  std::vector<ms_kernel_time> acc;
+  for (auto& r : g_prof_recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    bool found = false;
+    for (auto& k : acc)
+      if (std::strcmp(k.name, r.name) == 0) {
+        k.launches += 1;
+        k.total_ms += ms;
+        found = true;
+      }
+    if (!found) {
+      ms_kernel_time k{};
+      std::strncpy(k.name, r.name, sizeof(k.name) - 1);
+      k.launches = 1;
+      k.total_ms = ms;
+      acc.push_back(k);
+    }
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  int n = 0;
+  for (auto& k : acc)
+    if (n < max && out) out[n++] = k;
+  return (int)acc.size();
+}
 
 int num_sms() {
   static int sms[64] = {0};
@@ -43,7 +119,7 @@ static uint64_t n_items_hint(const OutView& o) {
 cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s) {
   auto k = engine_kernel<ColSource>;
   int grid = persistent_grid(k, kThreads, n_items_hint(out));
-  count_launch();
+  ProfScope prof_("engine_col", s);
   k<<<grid, kThreads, 0, s>>>(ColSource{src}, out, err);
   return cudaGetLastError();
 }
@@ -53,7 +129,7 @@ cudaError_t launch_engine_bitmask(const uint32_t* bits, const uint64_t* tile_off
                                   cudaStream_t s) {
   auto k = engine_kernel<BitmaskSource>;
   int grid = persistent_grid(k, kThreads, n_items_hint(out));
-  count_launch();
+  ProfScope prof_("engine_bitmask", s);
   k<<<grid, kThreads, 0, s>>>(BitmaskSource{bits, tile_off, start_tile, n_words, row_offset}, out, err);
   return cudaGetLastError();
 }
@@ -62,7 +138,7 @@ cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64
                                  uint32_t* err, cudaStream_t s) {
   auto k = engine_kernel<GatherSource>;
   int grid = persistent_grid(k, kThreads, n_items_hint(out));
-  count_launch();
+  ProfScope prof_("engine_gather", s);
   k<<<grid, kThreads, 0, s>>>(GatherSource{pos, data, row_offset}, out, err);
   return cudaGetLastError();
 }
@@ -81,20 +157,23 @@ struct BitmapPred {
   }
 };
 
-// Vector-register core of select: per tile of 2048 rows, decode,
-// evaluate the predicate, ballot -> one 32-bit mask word per 32 rows, popc.
+// Generic select core for formats without a fast path (DELTA_BP, RLE, block
+// sizes < 512): per tile of 2048 rows, decode into shared memory, evaluate the
+// predicate, ballot -> one 32-bit mask word per 32 rows; per 512-row segment
+// write count | (1-based last matching row << 16). Only segments in [s0, s1)
+// are written (the fast kernel covers the others).
 template <class Pred>
-__global__ void __launch_bounds__(kThreads) select_tiles_kernel(ColView c, Pred pred, uint32_t* bits,
-                                                                uint32_t* tile_count, uint32_t* tile_last,
-                                                                uint64_t n_tiles) {
+__global__ void __launch_bounds__(kThreads) select_generic_kernel(ColView c, Pred pred, uint32_t* bits,
+                                                                  uint32_t* seg_info, uint64_t s0, uint64_t s1) {
   __shared__ EngineSmem sm;
-  __shared__ uint32_t wcnt[kThreads / 32], wlast[kThreads / 32];
+  __shared__ uint32_t words[kChunk / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  const uint64_t t0 = (s0 * kSegRows) / kChunk;
+  const uint64_t t1 = (s1 * kSegRows + kChunk - 1) / kChunk;
+  for (uint64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
     const uint64_t r0 = t * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
     load_rows(c, r0, cnt, sm);
-    uint32_t cw_ = 0, last = 0;
     constexpr int kWordsPerWarp = kChunk / 32 / (kThreads / 32);
 #pragma unroll
     for (int q = 0; q < kWordsPerWarp; ++q) {
@@ -102,40 +181,69 @@ __global__ void __launch_bounds__(kThreads) select_tiles_kernel(ColView c, Pred 
       const uint32_t i = m * 32 + lane;
       const bool p = i < cnt && pred(sm.vals[i]);
       const uint32_t word = __ballot_sync(kFull, p);
-      if (lane == 0) bits[t * (kChunk / 32) + m] = word;
-      cw_ += __popc(word);
-      if (word) last = m * 32 + 32 - __clz(word);  // 1-based local row of the last match
-    }
-    if (lane == 0) {
-      wcnt[wid] = cw_;
-      wlast[wid] = last;
+      if (lane == 0) words[m] = word;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tot = 0, lst = 0;
-      for (int k = 0; k < kThreads / 32; ++k) {
-        tot += wcnt[k];
-        lst = wlast[k] > lst ? wlast[k] : lst;
+    constexpr int kSegsPerTile = kChunk / kSegRows;
+    if (wid < kSegsPerTile) {
+      const uint64_t sg = t * kSegsPerTile + wid;
+      if (sg >= s0 && sg < s1) {
+        const uint32_t my = lane < kSegWords ? words[wid * kSegWords + lane] : 0u;
+        if (lane < kSegWords) bits[sg * kSegWords + lane] = my;
+        const uint32_t cnt_ = (uint32_t)warp_sum(__popc(my));
+        const uint32_t last = (uint32_t)warp_max(my ? lane * 32 + 32 - __clz(my) : 0u);
+        if (lane == 0) seg_info[sg] = cnt_ | (last << 16);
       }
-      tile_count[t] = tot;
-      tile_last[t] = lst;
     }
     __syncthreads();
   }
 }
 
-cudaError_t launch_select_tiles(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* tile_count,
-                                uint32_t* tile_last, uint64_t n_tiles, cudaStream_t s) {
-  if (n_tiles == 0) return cudaSuccess;
-  count_launch();
-  if (p.is_bitmap) {
-    auto k = select_tiles_kernel<BitmapPred>;
-    k<<<persistent_grid(k, kThreads, n_tiles), kThreads, 0, s>>>(c, BitmapPred{p.bitmap, p.bitmap_bits}, bits,
-                                                                 tile_count, tile_last, n_tiles);
-  } else {
-    auto k = select_tiles_kernel<RangePred>;
-    k<<<persistent_grid(k, kThreads, n_tiles), kThreads, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits,
-                                                                 tile_count, tile_last, n_tiles);
+cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
+                          cudaStream_t s) {
+  if (NS == 0) return cudaSuccess;
+  // fast path: UNCOMPR, STATIC_BP, DYN_BP / FOR_BP with B >= 512, on full 512-row segments
+  int kind = -1;
+  uint64_t ns_fast = 0;
+  if (c.format == MS_UNCOMPR) { kind = FAST_UNCOMPR; ns_fast = c.n / kSegRows; }
+  if (c.format == MS_STATIC_BP) { kind = FAST_STATIC; ns_fast = c.n / kSegRows; }
+  if ((c.format == MS_DYN_BP || c.format == MS_FOR_BP) && c.B >= (uint32_t)kSegRows) {
+    kind = FAST_BLOCK;
+    ns_fast = (c.nb << c.log2B) / kSegRows;
+  }
+  if (kind >= 0 && ns_fast) {
+    FastPred fp{p.lo, p.span, p.neg, (uint32_t)p.is_bitmap, p.bitmap, p.bitmap_bits};
+    const size_t smem = (size_t)kFastWarps * kStages * kBufU32 * 4;
+    auto pick = [&](auto k) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFastWarps * 32, smem);
+      if (per_sm < 1) per_sm = 1;
+      const uint64_t warps = (uint64_t)per_sm * num_sms() * kFastWarps;
+      const uint64_t spw = (ns_fast + warps - 1) / warps;
+      const uint64_t used = (ns_fast + spw - 1) / spw;
+      const int grid = (int)((used + kFastWarps - 1) / kFastWarps);
+      ProfScope prof_("select_fast", s);
+      k<<<grid, kFastWarps * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw);
+    };
+    if (kind == FAST_UNCOMPR) pick(select_fast_kernel<FAST_UNCOMPR>);
+    else if (kind == FAST_STATIC) pick(select_fast_kernel<FAST_STATIC>);
+    else pick(select_fast_kernel<FAST_BLOCK>);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (ns_fast < NS) {  // the rest (other formats, partial segments, block remainders)
+    const uint64_t tiles = ((NS * kSegRows + kChunk - 1) / kChunk) - (ns_fast * kSegRows) / kChunk;
+    ProfScope prof_("select_generic", s);
+    if (p.is_bitmap) {
+      auto k = select_generic_kernel<BitmapPred>;
+      k<<<persistent_grid(k, kThreads, tiles), kThreads, 0, s>>>(c, BitmapPred{p.bitmap, p.bitmap_bits}, bits,
+                                                                 seg_info, ns_fast, NS);
+    } else {
+      auto k = select_generic_kernel<RangePred>;
+      k<<<persistent_grid(k, kThreads, tiles), kThreads, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits,
+                                                                 seg_info, ns_fast, NS);
+    }
   }
   return cudaGetLastError();
 }
@@ -172,14 +280,19 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(In in, Epi epi, uint64_t
     }
     __syncthreads();
     uint64_t off = s_E + ex;
+    uint64_t key = 0;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
       if (base + q < N) {
         epi(base + q, off, v[q]);
+        const uint64_t kq = epi.key(base + q);
+        key = kq > key ? kq : key;
         if (base + q == N - 1) epi.total(off + v[q]);
       }
       off += v[q];
     }
+    key = warp_max(key);
+    if ((tid & 31) == 0 && key) epi.max_key(key);
     __syncthreads();
   }
 }
@@ -188,7 +301,7 @@ template <class In, class Epi>
 static cudaError_t run_scan(In in, Epi epi, uint64_t N, uint64_t* status, uint32_t* ticket, cudaStream_t s) {
   if (N == 0) return cudaSuccess;
   auto k = scan_kernel<In, Epi>;
-  count_launch();
+  ProfScope prof_("scan", s);
   k<<<persistent_grid(k, kThreads, (N + kChunk - 1) / kChunk), kThreads, 0, s>>>(in, epi, N, status, ticket);
   return cudaGetLastError();
 }
@@ -197,33 +310,44 @@ struct U32In {
   const uint32_t* p;
   __device__ uint64_t operator()(uint64_t i) const { return p[i]; }
 };
-
-// select: tile offsets, output item -> start tile, max position
-struct TileEpi {
-  uint64_t* tile_off;
-  uint32_t* start_tile;
-  const uint32_t* tile_last;
-  unsigned long long* max_pos;
-  uint64_t row_offset;
-  uint64_t T;
-  __device__ void operator()(uint64_t idx, uint64_t off, uint64_t c) const {
-    tile_off[idx] = off;
-    if (c) {
-      for (uint64_t k = (off + kChunk - 1) / kChunk; k * kChunk < off + c; ++k) start_tile[k] = (uint32_t)idx;
-      atomicMax(max_pos, (unsigned long long)(row_offset + idx * kChunk + tile_last[idx] - 1));
-    }
-  }
-  __device__ void total(uint64_t t) const { tile_off[T] = t; }
+struct SegIn {  // seg_info: count in the low 16 bits
+  const uint32_t* p;
+  __device__ uint64_t operator()(uint64_t i) const { return p[i] & 0xffffu; }
+};
+struct NoKey {
+  __device__ uint64_t key(uint64_t) const { return 0; }
+  __device__ void max_key(uint64_t) const {}
 };
 
-cudaError_t launch_tile_scan(const uint32_t* tile_count, const uint32_t* tile_last, uint64_t T,
-                             uint64_t row_offset, uint64_t* tile_off, uint32_t* start_tile,
-                             unsigned long long* max_pos, uint64_t* status, uint32_t* ticket, cudaStream_t s) {
-  return run_scan(U32In{tile_count}, TileEpi{tile_off, start_tile, tile_last, max_pos, row_offset, T}, T, status,
+// select: segment offsets, output item -> start segment, 1 + max position
+struct SegEpi {
+  uint64_t* seg_off;
+  uint32_t* start_seg;
+  const uint32_t* seg_info;
+  unsigned long long* max_pos1;  // 1 + largest selected position (0 if none)
+  uint64_t row_offset;
+  uint64_t NS;
+  __device__ void operator()(uint64_t idx, uint64_t off, uint64_t c) const {
+    seg_off[idx] = off;
+    if (c)
+      for (uint64_t k = (off + kChunk - 1) / kChunk; k * kChunk < off + c; ++k) start_seg[k] = (uint32_t)idx;
+  }
+  __device__ uint64_t key(uint64_t idx) const {
+    const uint32_t last = seg_info[idx] >> 16;
+    return last ? row_offset + idx * kSegRows + last : 0;
+  }
+  __device__ void max_key(uint64_t k) const { atomicMax(max_pos1, (unsigned long long)k); }
+  __device__ void total(uint64_t t) const { seg_off[NS] = t; }
+};
+
+cudaError_t launch_seg_scan(const uint32_t* seg_info, uint64_t NS, uint64_t row_offset, uint64_t* seg_off,
+                            uint32_t* start_seg, unsigned long long* max_pos1, uint64_t* status, uint32_t* ticket,
+                            cudaStream_t s) {
+  return run_scan(SegIn{seg_info}, SegEpi{seg_off, start_seg, seg_info, max_pos1, row_offset, NS}, NS, status,
                   ticket, s);
 }
 
-struct CountEpi {
+struct CountEpi : NoKey {
   uint64_t* off;
   uint64_t T;
   __device__ void operator()(uint64_t idx, uint64_t o, uint64_t c) const { off[idx] = o; }
@@ -232,7 +356,7 @@ struct CountEpi {
 
 cudaError_t launch_count_scan(const uint32_t* counts, uint64_t T, uint64_t* off, uint64_t* status,
                               uint32_t* ticket, cudaStream_t s) {
-  return run_scan(U32In{counts}, CountEpi{off, T}, T, status, ticket, s);
+  return run_scan(U32In{counts}, CountEpi{{}, off, T}, T, status, ticket, s);
 }
 
 // RLE: run starts = exclusive prefix of the lengths; lengths must be >= 1 and
@@ -241,7 +365,7 @@ struct LenIn {
   const uint64_t* payload;
   __device__ uint64_t operator()(uint64_t i) const { return payload[2 * i + 1]; }
 };
-struct StartsEpi {
+struct StartsEpi : NoKey {
   uint64_t* starts;
   uint64_t R, n;
   uint32_t* err;
@@ -257,7 +381,7 @@ struct StartsEpi {
 
 cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
                               uint32_t* ticket, uint32_t* err, cudaStream_t s) {
-  return run_scan(LenIn{payload}, StartsEpi{starts, R, n, err}, R, status, ticket, s);
+  return run_scan(LenIn{payload}, StartsEpi{{}, starts, R, n, err}, R, status, ticket, s);
 }
 
 __global__ void chunk_run_kernel(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run) {
@@ -271,7 +395,7 @@ __global__ void chunk_run_kernel(const uint64_t* starts, uint64_t R, uint64_t n,
 
 cudaError_t launch_chunk_run(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run, cudaStream_t s) {
   if (R == 0) return cudaSuccess;
-  count_launch();
+  ProfScope prof_("chunk_run", s);
   chunk_run_kernel<<<num_sms() * 8, 256, 0, s>>>(starts, R, n, chunk_run);
   return cudaGetLastError();
 }
@@ -302,7 +426,7 @@ __global__ void __launch_bounds__(kThreads) rle_count_kernel(const uint64_t* __r
 cudaError_t launch_rle_count(const uint64_t* v, uint64_t n, uint32_t* counts, cudaStream_t s) {
   const uint64_t T = (n + kChunk - 1) / kChunk;
   if (!T) return cudaSuccess;
-  count_launch();
+  ProfScope prof_("rle_count", s);
   rle_count_kernel<<<persistent_grid(rle_count_kernel, kThreads, T), kThreads, 0, s>>>(v, n, counts);
   return cudaGetLastError();
 }
@@ -339,7 +463,7 @@ cudaError_t launch_rle_write(const uint64_t* v, uint64_t n, const uint64_t* chun
                              uint64_t* starts, cudaStream_t s) {
   const uint64_t T = (n + kChunk - 1) / kChunk;
   if (!T) return cudaSuccess;
-  count_launch();
+  ProfScope prof_("rle_write", s);
   rle_write_kernel<<<persistent_grid(rle_write_kernel, kThreads, T), kThreads, 0, s>>>(v, n, chunk_off, payload,
                                                                                         starts);
   return cudaGetLastError();
@@ -353,7 +477,7 @@ __global__ void rle_len_kernel(const uint64_t* starts, uint64_t R, uint64_t n, u
 
 cudaError_t launch_rle_len(const uint64_t* starts, uint64_t R, uint64_t n, uint64_t* payload, cudaStream_t s) {
   if (!R) return cudaSuccess;
-  count_launch();
+  ProfScope prof_("rle_len", s);
   rle_len_kernel<<<num_sms() * 8, 256, 0, s>>>(starts, R, n, payload);
   return cudaGetLastError();
 }
@@ -408,7 +532,7 @@ __global__ void __launch_bounds__(kThreads) sum_kernel(ColView c, unsigned long 
 }
 
 cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err, cudaStream_t s) {
-  count_launch();
+  ProfScope prof_("sum", s);
   sum_kernel<<<persistent_grid(sum_kernel, kThreads, ~0ull), kThreads, 0, s>>>(c, out);
   return cudaGetLastError();
 }
@@ -445,7 +569,7 @@ cudaError_t launch_sum_at(const ColView& data, const ColView& pos, uint64_t row_
                           uint32_t* err, cudaStream_t s) {
   const uint64_t T = (pos.n + kChunk - 1) / kChunk;
   if (!T) return cudaSuccess;
-  count_launch();
+  ProfScope prof_("sum_at", s);
   sum_at_kernel<<<persistent_grid(sum_at_kernel, kThreads, T), kThreads, 0, s>>>(data, pos, row_offset, out, err);
   return cudaGetLastError();
 }
@@ -491,7 +615,7 @@ cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t
                                unsigned long long* sums, uint32_t* err, cudaStream_t s) {
   const uint64_t T = (gid.n + kChunk - 1) / kChunk;
   if (!T) return cudaSuccess;
-  count_launch();
+  ProfScope prof_("sum_grouped", s);
   sum_grouped_kernel<<<persistent_grid(sum_grouped_kernel, kThreads, T), kThreads, 0, s>>>(gid, vals, n_groups,
                                                                                           sums, err);
   return cudaGetLastError();

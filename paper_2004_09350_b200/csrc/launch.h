@@ -10,9 +10,23 @@ namespace ms {
 struct ColView;
 struct OutView;
 
-// instrumentation: kernel launches issued by this library
+// instrumentation: kernel launches issued by this library, optional event timing
 void count_launch();
 uint64_t launch_count();
+class ProfScope {  // counts one launch; brackets it with events when profiling is on
+ public:
+  ProfScope(const char* name, cudaStream_t s);
+  ~ProfScope();
+
+ private:
+  const char* name_;
+  cudaStream_t s_;
+  bool on_;
+  void* a_ = nullptr;
+  void* b_ = nullptr;
+};
+void profile_enable(int on);
+int profile_read(ms_kernel_time* out, int max);
 
 // predicate in the range form keep = ((v - lo) <= span) != neg, or a bitmap
 struct PredSpec {
@@ -30,12 +44,13 @@ cudaError_t launch_engine_bitmask(const uint32_t* bits, const uint64_t* tile_off
 cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64_t row_offset, const OutView& out,
                                  uint32_t* err, cudaStream_t s);
 
-cudaError_t launch_select_tiles(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* tile_count,
-                                uint32_t* tile_last, uint64_t n_tiles, cudaStream_t s);
-// exclusive scan of per-tile counts -> tile_off[0..T], start_tile[], max position
-cudaError_t launch_tile_scan(const uint32_t* tile_count, const uint32_t* tile_last, uint64_t T,
-                             uint64_t row_offset, uint64_t* tile_off, uint32_t* start_tile,
-                             unsigned long long* max_pos, uint64_t* status, uint32_t* ticket, cudaStream_t s);
+// select core: bit mask (16 words per 512-row segment) + seg_info (count | last << 16)
+cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
+                          cudaStream_t s);
+// exclusive scan of per-segment counts -> seg_off[0..NS], start_seg[] per output item, 1 + max position
+cudaError_t launch_seg_scan(const uint32_t* seg_info, uint64_t NS, uint64_t row_offset, uint64_t* seg_off,
+                            uint32_t* start_seg, unsigned long long* max_pos1, uint64_t* status, uint32_t* ticket,
+                            cudaStream_t s);
 // RLE run starts (exclusive prefix of lengths), validation against n
 cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
                               uint32_t* ticket, uint32_t* err, cudaStream_t s);

@@ -107,6 +107,8 @@ def _load():
         "ms_status_str": ([ctypes.c_int], ctypes.c_char_p),
         "ms_abi_version": ([], ctypes.c_int),
         "ms_launch_count": ([], u64),
+        "ms_profile_enable": ([ctypes.c_int], None),
+        "ms_profile_read": ([vp, ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -319,6 +321,22 @@ def check_errors(stream=None):
 
 def launch_count() -> int:
     return int(_lib.ms_launch_count())
+
+
+class _KernelTime(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 48), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double)]
+
+
+def profile_enable(on: bool = True):
+    """Bracket every libms kernel launch with CUDA events on its stream."""
+    _lib.ms_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total ms)} since the last read (waits for the events)."""
+    buf = (_KernelTime * 64)()
+    k = _lib.ms_profile_read(buf, 64)
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(min(k, 64))}
 
 
 def u64(t: torch.Tensor) -> int:
