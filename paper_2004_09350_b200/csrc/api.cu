@@ -565,13 +565,14 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t n = in->n;
   const uint64_t NS = (n + kSegRows - 1) / kSegRows;  // 512-row segments
   const uint64_t n_words = NS * kSegWords;
-  const uint64_t items_max = (n + kChunk - 1) / kChunk + 1;
+  const uint32_t G = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;  // output item size
+  const uint64_t items_max = (n + G - 1) / G + 1;
   Scratch sc(ctx);
   const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] 1 + max position
   const uint64_t o_bits = sc.add(4 * n_words, false);
   const uint64_t o_seg = sc.add(4 * (NS + 1), false);
   const uint64_t o_off = sc.add(8 * (NS + 1), true);
-  const uint64_t o_start = sc.add(4 * (items_max + 1), false);
+  const uint64_t o_gs = sc.add(8 * (items_max + 1), false);
   const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
   const uint64_t o_tk1 = sc.add(8, true);
   const uint64_t o_st2 = sc.add(8 * (items_max + 1), true);
@@ -584,9 +585,9 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
   uint64_t* seg_off = sc.at<uint64_t>(o_off);
   MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, ctx.s));
-  MS_TRY_CUDA(launch_seg_scan(sc.at<uint32_t>(o_seg), NS, row_offset, seg_off, sc.at<uint32_t>(o_start),
-                              sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1),
-                              ctx.s));
+  MS_TRY_CUDA(launch_seg_scan(sc.at<uint32_t>(o_seg), sc.at<uint32_t>(o_bits), NS, row_offset, G, seg_off,
+                              sc.at<uint64_t>(o_gs), sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1),
+                              sc.at<uint32_t>(o_tk1), ctx.s));
   uint64_t h[3] = {0, 0, 0};
   if (NS) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], seg_off + NS, 8, cudaMemcpyDeviceToHost, ctx.s));
   MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
@@ -624,16 +625,27 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   if (is_block(f.format) && 64 * (n_out / f.block_size) > 0xffffffffull) return MS_E_INVALID;
   MS_TRY(alloc_column(ctx, out, f, n_out, cap, f.format == MS_RLE ? n_out : 0));
   if (f.format == MS_UNCOMPR || f.format == MS_RLE || f.format == MS_STATIC_BP) out->payload_words = cap;
+  if (is_block(f.format)) {
+    cudaError_t e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
+    if (e != cudaSuccess) { release(ctx, out); return cuda_status(e); }
+  }
   if (n_out) {
-    OutView ov = out_view(out, sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2));
-    cudaError_t e = launch_engine_bitmask(sc.at<uint32_t>(o_bits), seg_off, sc.at<uint32_t>(o_start), n_words,
-                                          row_offset, ov, err, ctx.s);
+    PosEnc pe{};
+    pe.format = f.format;
+    pe.w = f.bit_width;
+    pe.G = G;
+    pe.log2G = log2u(G);
+    pe.n_out = n_out;
+    pe.payload = out->payload;
+    pe.cw = out->cw;
+    pe.ref = out->ref;
+    pe.rem = out->rem;
+    cudaError_t e = launch_positions(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
+                                     sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
     if (e != cudaSuccess) {
       release(ctx, out);
       return cuda_status(e);
     }
-  } else if (is_block(f.format)) {
-    cudaMemsetAsync(out->cw, 0, 4, ctx.s);
   }
   ms_status st = finish_output(ctx, out, err);
   if (st == MS_OK) st = maybe_shrink(ctx, out);
@@ -652,7 +664,7 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
   Ctx ctx(ctx_);
   const uint64_t n = positions->n;
   if (is_block(out_fmt.format) && 64 * (n / out_fmt.block_size) > 0xffffffffull) return MS_E_INVALID;
-  const uint64_t items = (n + kChunk - 1) / kChunk;
+  const uint64_t items = (n + 127) / 128;  // enough for any item size (>= 128 rows)
   Scratch sc(ctx);
   const uint64_t o_meta = sc.add(64, true);
   const uint64_t o_st = sc.add(8 * (items + 1), true);
@@ -666,13 +678,49 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
   ColView pv = view_of(positions), dv = view_of(data);
   MS_TRY_CUDA(run_rle(sc, positions, rp_pos, pv, err));
   MS_TRY_CUDA(run_rle(sc, data, rp_data, dv, err));
-  auto launch = [&](const OutView& ov) { return launch_engine_gather(pv, dv, row_offset, ov, err, ctx.s); };
   uint64_t cap = 0;
   if (is_block(out_fmt.format)) {
     uint32_t wmax = 64;  // projected codes cannot be wider than a static data width
     if (data->fmt.format == MS_STATIC_BP && out_fmt.format != MS_DELTA_BP) wmax = data->fmt.bit_width;
     cap = (n / out_fmt.block_size) * (out_fmt.block_size / 64) * wmax;
   }
+  // warp pipeline (positions decoded block-aligned, data gathered with header broadcast)
+  const uint32_t G = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;
+  const int32_t pf = positions->fmt.format, df = data->fmt.format;
+  const bool pos_ok = pf == MS_UNCOMPR || pf == MS_STATIC_BP || pf == MS_DYN_BP || pf == MS_FOR_BP ||
+                      (pf == MS_DELTA_BP && positions->fmt.block_size == G);
+  const bool data_ok = df == MS_UNCOMPR || df == MS_STATIC_BP || df == MS_DYN_BP || df == MS_FOR_BP;
+  const bool out_ok = !(out_fmt.format == MS_STATIC_BP && out_fmt.bit_width == 0);
+  if (pos_ok && data_ok && out_ok) {
+    ms_fmt f = out_fmt;
+    if (f.format == MS_STATIC_BP) cap = words_for(n, f.bit_width);
+    if (f.format == MS_UNCOMPR) cap = n;
+    MS_TRY(alloc_column(ctx, out, f, n, cap, 0));
+    if (f.format == MS_UNCOMPR || f.format == MS_STATIC_BP) out->payload_words = cap;
+    cudaError_t e = cudaSuccess;
+    if (is_block(f.format)) e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
+    PosEnc pe{};
+    pe.format = f.format;
+    pe.w = f.bit_width;
+    pe.G = G;
+    pe.log2G = log2u(G);
+    pe.n_out = n;
+    pe.payload = out->payload;
+    pe.cw = out->cw;
+    pe.ref = out->ref;
+    pe.rem = out->rem;
+    if (e == cudaSuccess)
+      e = launch_project_warp(pv, dv, row_offset, pe, sc.at<uint64_t>(o_st), sc.at<uint32_t>(o_tk), err, ctx.s);
+    if (e != cudaSuccess) {
+      release(ctx, out);
+      return cuda_status(e);
+    }
+    ms_status st = finish_output(ctx, out, err);
+    if (st == MS_OK) st = maybe_shrink(ctx, out);
+    if (st != MS_OK) release(ctx, out);
+    return st;
+  }
+  auto launch = [&](const OutView& ov) { return launch_engine_gather(pv, dv, row_offset, ov, err, ctx.s); };
   return encode_into(ctx, sc, o_meta, o_st, o_tk, o_tk2, out_fmt, n, cap, launch, out);
 }
 

@@ -199,19 +199,57 @@ struct BitmaskSource {
 };
 
 // Gather through positions (project): rows of the positions column
-// give global positions p; the value is data[p - row_offset].
+// give global positions p; the value is data[p - row_offset]. For the O(1)
+// random-access formats each thread issues the header loads (cw, ref) of all
+// its positions, then all payload loads, so every thread has 8-16 independent
+// loads in flight instead of a dependent chain per position.
 struct GatherSource {
   ColView pos;
   ColView data;
   uint64_t row_offset;
   __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, EngineSmem& sm, uint32_t* err) const {
     load_rows(pos, r0, cnt, sm);
-    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-      const uint64_t p = sm.vals[i];
-      uint64_t v = 0;
-      if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
-      else v = read_row(data, p - row_offset);
-      sm.vals[i] = v;
+    const int tid = threadIdx.x;
+    if (data.format == MS_FOR_BP || data.format == MS_DYN_BP) {
+      const uint64_t main_rows = data.nb << data.log2B;
+      uint64_t r[kVPT], b[kVPT];
+      uint32_t cw0[kVPT], w[kVPT];
+      uint64_t rf[kVPT];
+      bool ok[kVPT];
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const uint32_t i = tid + q * kThreads;
+        const uint64_t p = i < cnt ? sm.vals[i] : row_offset;
+        ok[q] = i < cnt && p >= row_offset && p - row_offset < data.n;
+        if (i < cnt && !ok[q]) atomicOr(err, err_bit(MS_E_RANGE));
+        r[q] = ok[q] ? p - row_offset : 0;
+        b[q] = r[q] >> data.log2B;
+      }
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const bool inm = ok[q] && r[q] < main_rows;
+        cw0[q] = inm ? __ldg(data.cw + b[q]) : 0u;
+        w[q] = inm ? __ldg(data.cw + b[q] + 1) : 0u;
+        rf[q] = inm && data.format == MS_FOR_BP ? __ldg(data.ref + b[q]) : 0ull;
+        if (ok[q] && !inm) rf[q] = __ldg(data.rem + (r[q] - main_rows));
+      }
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const bool inm = ok[q] && r[q] < main_rows;
+        w[q] -= cw0[q];
+        const uint64_t bit = (uint64_t)cw0[q] * data.B + (uint64_t)(r[q] & (data.B - 1)) * w[q];
+        const uint64_t v = inm ? unpack_at(data.payload, bit, w[q]) : 0ull;
+        const uint32_t i = tid + q * kThreads;
+        if (i < cnt) sm.vals[i] = rf[q] + v;
+      }
+    } else {
+      for (uint32_t i = tid; i < cnt; i += kThreads) {
+        const uint64_t p = sm.vals[i];
+        uint64_t v = 0;
+        if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
+        else v = read_row(data, p - row_offset);
+        sm.vals[i] = v;
+      }
     }
     __syncthreads();
   }

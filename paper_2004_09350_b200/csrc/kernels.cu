@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "engine.cuh"
 #include "select_fast.cuh"
+#include "positions.cuh"
 #include "launch.h"
 
 namespace ms {
@@ -319,18 +320,32 @@ struct NoKey {
   __device__ void max_key(uint64_t) const {}
 };
 
-// select: segment offsets, output item -> start segment, 1 + max position
+// select: segment offsets, 1 + max position, and the first position of every
+// output item (G ranks) that starts inside a segment (select-in-segment on the mask)
 struct SegEpi {
   uint64_t* seg_off;
-  uint32_t* start_seg;
+  uint64_t* gstart;
   const uint32_t* seg_info;
+  const uint32_t* bits;
   unsigned long long* max_pos1;  // 1 + largest selected position (0 if none)
   uint64_t row_offset;
   uint64_t NS;
+  uint32_t G;
   __device__ void operator()(uint64_t idx, uint64_t off, uint64_t c) const {
     seg_off[idx] = off;
-    if (c)
-      for (uint64_t k = (off + kChunk - 1) / kChunk; k * kChunk < off + c; ++k) start_seg[k] = (uint32_t)idx;
+    if (!c) return;
+    for (uint64_t k = (off + G - 1) / G; k * G < off + c; ++k) {
+      uint32_t q = (uint32_t)(k * G - off);  // rank inside the segment
+      for (uint32_t wdi = 0; wdi < kSegWords; ++wdi) {
+        const uint32_t word = bits[idx * kSegWords + wdi];
+        const uint32_t pc = __popc(word);
+        if (q < pc) {
+          gstart[k] = row_offset + idx * kSegRows + wdi * 32 + select_bit(word, q);
+          break;
+        }
+        q -= pc;
+      }
+    }
   }
   __device__ uint64_t key(uint64_t idx) const {
     const uint32_t last = seg_info[idx] >> 16;
@@ -340,10 +355,10 @@ struct SegEpi {
   __device__ void total(uint64_t t) const { seg_off[NS] = t; }
 };
 
-cudaError_t launch_seg_scan(const uint32_t* seg_info, uint64_t NS, uint64_t row_offset, uint64_t* seg_off,
-                            uint32_t* start_seg, unsigned long long* max_pos1, uint64_t* status, uint32_t* ticket,
-                            cudaStream_t s) {
-  return run_scan(SegIn{seg_info}, SegEpi{seg_off, start_seg, seg_info, max_pos1, row_offset, NS}, NS, status,
+cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint64_t NS, uint64_t row_offset,
+                            uint32_t G, uint64_t* seg_off, uint64_t* gstart, unsigned long long* max_pos1,
+                            uint64_t* status, uint32_t* ticket, cudaStream_t s) {
+  return run_scan(SegIn{seg_info}, SegEpi{seg_off, gstart, seg_info, bits, max_pos1, row_offset, NS, G}, NS, status,
                   ticket, s);
 }
 
@@ -619,6 +634,40 @@ cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t
   sum_grouped_kernel<<<persistent_grid(sum_grouped_kernel, kThreads, T), kThreads, 0, s>>>(gid, vals, n_groups,
                                                                                           sums, err);
   return cudaGetLastError();
+}
+
+}  // namespace ms
+
+namespace ms {
+
+// ------------------------------------------------- select output encoder
+template <class Src>
+static cudaError_t run_warp_encode(const Src& src, const PosEnc& e, uint64_t* status, uint32_t* ticket,
+                                   uint32_t* err, const char* name, cudaStream_t s) {
+  const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
+  if (!n_items) return cudaSuccess;
+  auto k = warp_encode_kernel<Src>;
+  const size_t smem = (size_t)kEncWarps * e.G * 8;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kEncWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)per_sm * num_sms();
+  const uint64_t need = (n_items + kEncWarps - 1) / kEncWarps;
+  if (need < grid) grid = need;
+  ProfScope prof_(name, s);
+  k<<<(int)grid, kEncWarps * 32, smem, s>>>(src, e, n_items, status, ticket, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                             uint64_t row_offset, uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {
+  return run_warp_encode(MaskSource{bits, NS, gstart, row_offset}, e, status, ticket, err, "pos_encode", s);
+}
+
+cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
+                                uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {
+  return run_warp_encode(ProjectSource{pos, data, row_offset}, e, status, ticket, err, "project_warp", s);
 }
 
 }  // namespace ms

@@ -48,9 +48,27 @@ cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
                           cudaStream_t s);
 // exclusive scan of per-segment counts -> seg_off[0..NS], start_seg[] per output item, 1 + max position
-cudaError_t launch_seg_scan(const uint32_t* seg_info, uint64_t NS, uint64_t row_offset, uint64_t* seg_off,
-                            uint32_t* start_seg, unsigned long long* max_pos1, uint64_t* status, uint32_t* ticket,
-                            cudaStream_t s);
+// ... and, for every output item of G ranks starting in a segment, the item's first position
+cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint64_t NS, uint64_t row_offset,
+                            uint32_t G, uint64_t* seg_off, uint64_t* gstart, unsigned long long* max_pos1,
+                            uint64_t* status, uint32_t* ticket, cudaStream_t s);
+// select output encoder (positions.cuh): E1, cw scan, E2
+struct PosEnc {  // output of the warp encoder
+  int32_t format;      // output format
+  uint32_t w;          // STATIC_BP width
+  uint32_t G, log2G;   // item size: B for block formats, 512 otherwise
+  uint64_t n_out;      // output length
+  uint64_t* payload;
+  uint32_t* cw;
+  uint64_t* ref;
+  uint64_t* rem;
+};
+cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                             uint64_t row_offset, uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);
+// project through the warp encoder (positions DELTA_BP with B == G, or O(1) formats; data O(1) formats)
+cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
+                                uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);
+
 // RLE run starts (exclusive prefix of lengths), validation against n
 cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
                               uint32_t* ticket, uint32_t* err, cudaStream_t s);

@@ -1,0 +1,291 @@
+// positions.cuh — output-side buffer layer of select: turn the
+// select bit mask into the positions column in any output format.
+//
+// Output ranks are cut into items of G ranks: G = B for block formats (one
+// item = one output block), G = 512 otherwise. The segment scan that computes
+// each segment's output rank also finds, for every item starting inside the
+// segment, the item's first position (gstart). The encoder then runs one warp
+// per item, items taken in order from a ticket: expand the item's positions
+// from the mask starting at gstart into a shared-memory tile (the paper's
+// L1-resident output buffer), compute the block's width (DELTA: widest
+// difference, FOR: ebw(max - min), DYN: ebw(max)), get the exclusive
+// prefix of the widths by decoupled look-back (cw, D-4), pack and store whole
+// words. The final partial block goes to the uncompressed remainder.
+#pragma once
+#include "common.cuh"
+#include "launch.h"
+
+namespace ms {
+
+// select-in-word: position of the (k+1)-th set bit of x (k < popc(x))
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
+  for (uint32_t i = 0; i < k; ++i) x &= x - 1;
+  return __ffs(x) - 1;
+}
+
+// ------------------------------------------------------------------ sources
+// select: expand the item's positions from the mask, starting at gstart[item]
+struct MaskSource {
+  const uint32_t* bits;
+  uint64_t NS;
+  const uint64_t* gstart;
+  uint64_t row_offset;
+  __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, uint64_t* P, uint32_t lane,
+                                       uint32_t* err) const {
+    const uint64_t n_words = NS * kSegWords;
+    const uint64_t row = __ldg(gstart + item) - row_offset;
+    uint64_t wi = row >> 5;
+    uint32_t first_mask = ~0u << (row & 31);
+    uint32_t got = 0;
+    while (got < cnt && wi < n_words) {
+      uint32_t wv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t m = wi + q * 32 + lane;
+        wv[q] = m < n_words ? __ldg(bits + m) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t word = wv[q];
+        if (q == 0 && lane == 0) word &= first_mask;
+        const uint32_t pc = __popc(word);
+        uint32_t incl = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= (uint32_t)o) incl += t;
+        }
+        uint32_t k = got + incl - pc;
+        const uint64_t base = row_offset + (wi + q * 32 + lane) * 32;
+        while (word && k < cnt) {
+          const int b = __ffs(word) - 1;
+          word &= word - 1;
+          P[k++] = base + b;
+        }
+        got += __shfl_sync(kFull, incl, 31);
+      }
+      first_mask = ~0u;
+      wi += 128;
+    }
+    __syncwarp();
+  }
+};
+
+// project: decode the item's positions (ranks r0 .. r0+cnt of the
+// positions column), then gather data[p - row_offset] for each. Positions:
+// DELTA_BP with B == item size (block-aligned: warp prefix sum of the
+// deltas), or any O(1)-addressable format. Data: O(1) formats; the block
+// headers (cw, ref) of the data window are loaded once per warp (lane j ->
+// block b_lo + j) and broadcast by shuffles; each lane then has its 16
+// payload loads in flight at once.
+struct ProjectSource {
+  ColView pos;
+  ColView data;
+  uint64_t row_offset;
+  __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, uint64_t* P, uint32_t lane,
+                                       uint32_t* err) const {
+    // ---- positions
+    if (pos.format == MS_DELTA_BP && r0 + cnt <= (pos.nb << pos.log2B)) {  // block-aligned: B == G (host checks)
+      const uint64_t b = r0 >> pos.log2B;
+      const uint32_t cw0 = __ldg(pos.cw + b);
+      const uint32_t w = __ldg(pos.cw + b + 1) - cw0;
+      const uint64_t bit0 = (uint64_t)cw0 * pos.B;
+      const uint32_t per = pos.B / 32;  // consecutive codes per lane
+      uint64_t acc = 0;
+      for (uint32_t q = 0; q < per; ++q) {
+        acc += unpack_at(pos.payload, bit0 + (uint64_t)(lane * per + q) * w, w);
+        P[lane * per + q] = acc;
+      }
+      uint64_t incl = warp_incl_scan(acc);
+      const uint64_t base = __ldg(pos.ref + b) + incl - acc;
+      __syncwarp();
+      for (uint32_t q = 0; q < per; ++q) P[lane * per + q] += base;
+    } else {
+      for (uint32_t i = lane; i < cnt; i += 32) P[i] = read_row(pos, r0 + i);
+    }
+    __syncwarp();
+    // ---- gather
+    if (data.format == MS_DYN_BP || data.format == MS_FOR_BP) {
+      const uint64_t main_rows = data.nb << data.log2B;
+      const uint64_t plo = P[0] - row_offset, phi = P[cnt - 1] - row_offset;  // sorted positions
+      const uint64_t b_lo = plo >> data.log2B;
+      const bool window = P[0] >= row_offset && phi < main_rows && ((phi >> data.log2B) - b_lo) < 32 &&
+                          P[cnt - 1] >= P[0];
+      uint32_t h_cw = 0;
+      uint64_t h_ref = 0;
+      if (window) {
+        const uint64_t bj = b_lo + lane;
+        if (bj <= data.nb) h_cw = __ldg(data.cw + bj);
+        if (bj < data.nb && data.format == MS_FOR_BP) h_ref = __ldg(data.ref + bj);
+      }
+      const uint32_t h_cw_next = __shfl_down_sync(kFull, h_cw, 1);
+      uint32_t h_last = 0;
+      if (window) {
+        const uint64_t bj = b_lo + 32;
+        h_last = (lane == 31 && bj <= data.nb) ? __ldg(data.cw + bj) : 0u;
+      }
+      const uint32_t h_cw1 = lane == 31 ? h_last : h_cw_next;
+      for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * 8) {
+        uint64_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t i = i0 + q * 32 + lane;
+          const uint64_t p = i < cnt ? P[i] : row_offset;
+          const bool ok = p >= row_offset && p - row_offset < data.n;
+          if (i < cnt && !ok) atomicOr(err, err_bit(MS_E_RANGE));
+          const uint64_t r = ok ? p - row_offset : 0;
+          const uint64_t b = r >> data.log2B;
+          uint32_t cw0 = 0, w = 0;
+          uint64_t rf = 0;
+          const bool in_win = window && b >= b_lo && b - b_lo < 32 && r < main_rows;  // (unsorted positions)
+          if (window) {
+            const int src = (int)(b - b_lo) & 31;
+            cw0 = __shfl_sync(kFull, h_cw, src);
+            w = __shfl_sync(kFull, h_cw1, src) - cw0;
+            rf = __shfl_sync(kFull, h_ref, src);
+          }
+          if (in_win) {
+          } else if (r < main_rows) {
+            cw0 = __ldg(data.cw + b);
+            w = __ldg(data.cw + b + 1) - cw0;
+            rf = data.format == MS_FOR_BP ? __ldg(data.ref + b) : 0ull;
+          } else {
+            cw0 = 0; w = 0;
+            rf = __ldg(data.rem + (r - main_rows));
+          }
+          if (data.format == MS_DYN_BP) rf = (r < main_rows) ? 0ull : rf;
+          v[q] = rf + unpack_at(data.payload, (uint64_t)cw0 * data.B + (r & (data.B - 1)) * (uint64_t)w, w);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t i = i0 + q * 32 + lane;
+          if (i < cnt) P[i] = v[q];
+        }
+      }
+    } else {
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        const uint64_t p = P[i];
+        uint64_t v = 0;
+        if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
+        else v = read_row(data, p - row_offset);
+        P[i] = v;
+      }
+    }
+    __syncwarp();
+  }
+};
+
+// Output-side buffer layer, one warp per item (G output rows). Dynamic shared
+// memory: warps x G uint64. The Source fills P[0..cnt) with the item's values.
+constexpr int kEncWarps = 4;
+template <class Src>
+__global__ void __launch_bounds__(kEncWarps * 32) warp_encode_kernel(Src src, PosEnc e, uint64_t n_items,
+                                                                     uint64_t* status, uint32_t* ticket, uint32_t* err) {
+  extern __shared__ __align__(16) uint64_t enc_sm[];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t* P = enc_sm + (uint64_t)wid * e.G;
+  const bool is_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  while (true) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(ticket, 1u);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= n_items) break;
+    const uint64_t r0 = (uint64_t)item * e.G;
+    const uint32_t cnt = (uint32_t)min((uint64_t)e.G, e.n_out - r0);
+    src.load(item, r0, cnt, P, lane, err);
+    if (!is_block) {
+      if (e.format == MS_UNCOMPR) {
+        for (uint32_t i = lane; i < cnt; i += 32) e.payload[r0 + i] = P[i];
+      } else if (e.format == MS_RLE) {
+        for (uint32_t i = lane; i < cnt; i += 32) {
+          e.payload[2 * (r0 + i)] = P[i];
+          e.payload[2 * (r0 + i) + 1] = 1;
+        }
+      } else {  // STATIC_BP: item = ranks [512k, 512k+cnt) at bit 512k*w (word aligned)
+        const uint32_t w = e.w;
+        const uint64_t mask = low_mask(w);
+        const uint64_t wbase = (uint64_t)item * 8 * w;
+        const uint32_t nwords = (uint32_t)(((uint64_t)cnt * w + 63) / 64);
+        for (uint32_t m = lane; m < nwords; m += 32) {
+          const uint64_t bit0 = (uint64_t)m * 64;
+          uint32_t j = (uint32_t)(bit0 / w);
+          const uint32_t sft = (uint32_t)(bit0 - (uint64_t)j * w);
+          uint64_t acc = (P[j] & mask) >> sft;
+          for (++j; j < cnt; ++j) {
+            const uint64_t jb = (uint64_t)j * w;
+            if (jb >= bit0 + 64) break;
+            acc |= (P[j] & mask) << (jb - bit0);
+          }
+          e.payload[wbase + m] = acc;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (cnt < e.G) {  // final partial block -> uncompressed remainder
+      for (uint32_t i = lane; i < cnt; i += 32) e.rem[i] = P[i];
+      __syncwarp();
+      continue;
+    }
+    // ---- block width
+    uint64_t mx = 0, rmin = 0;
+    if (e.format == MS_DELTA_BP) {
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        const uint64_t d = i ? P[i] - P[i - 1] : 0ull;
+        mx = d > mx ? d : mx;
+      }
+      mx = warp_max(mx);
+    } else {  // FOR: ebw(max - min); DYN: ebw(max) (values need not be sorted: project)
+      uint64_t lo = ~0ull, hi = 0;
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        lo = P[i] < lo ? P[i] : lo;
+        hi = P[i] > hi ? P[i] : hi;
+      }
+      hi = warp_max(hi);
+      if (e.format == MS_FOR_BP) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t t = __shfl_xor_sync(kFull, lo, o);
+          lo = t < lo ? t : lo;
+        }
+        mx = hi - lo;
+        rmin = lo;
+      } else {
+        mx = hi;
+      }
+    }
+    const uint32_t w = ebw64(mx);
+    const uint64_t E = lookback_warp(status, item, w);
+    if (lane == 0) {
+      if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      e.cw[item + 1] = (uint32_t)(E + w);
+      if (e.format == MS_DELTA_BP) e.ref[item] = P[0];
+      if (e.format == MS_FOR_BP) e.ref[item] = rmin;
+    }
+    if (w) {
+      const uint64_t wbase = E * (e.G >> 6);
+      const uint32_t nwords = (e.G >> 6) * w;
+      const uint64_t rf = rmin;
+      for (uint32_t m = lane; m < nwords; m += 32) {
+        const uint64_t bit0 = (uint64_t)m * 64;
+        uint32_t j = (uint32_t)(bit0 / w);
+        const uint32_t sft = (uint32_t)(bit0 - (uint64_t)j * w);
+        auto code = [&](uint32_t i) -> uint64_t {
+          if (e.format == MS_DELTA_BP) return i ? P[i] - P[i - 1] : 0ull;
+          if (e.format == MS_FOR_BP) return P[i] - rf;
+          return P[i];
+        };
+        uint64_t acc = code(j) >> sft;
+        for (++j; j < cnt; ++j) {
+          const uint64_t jb = (uint64_t)j * w;
+          if (jb >= bit0 + 64) break;
+          acc |= code(j) << (jb - bit0);
+        }
+        e.payload[wbase + m] = acc;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace ms

@@ -181,71 +181,108 @@ __device__ __forceinline__ uint32_t seg_uncompr(const uint64_t* __restrict__ v, 
   return my;
 }
 
-// Per-warp contiguous range of full 512-row segments [s_begin, s_end).
+// ---- TMA bulk copy + mbarrier helpers (sm_90+; SASS UBLKCP / SYNCS)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// Per-warp contiguous range of full 512-row segments [s_begin, s_end). Lane 0
+// streams each segment's packed payload (64*w bytes, 64-byte aligned) into a
+// per-warp ring of kStages shared-memory slots with one TMA bulk copy, tracked
+// by one mbarrier per slot; the width / reference of the segment travel with
+// the slot, so decoding needs no further global reads.
 template <int KIND>
 __global__ void __launch_bounds__(kFastWarps * 32, 2) select_fast_kernel(ColView c, FastPred pred,
-                                                                     uint32_t* __restrict__ bits,
-                                                                     uint32_t* __restrict__ seg_info, uint64_t NS,
-                                                                     uint64_t spw) {
-  extern __shared__ __align__(16) uint32_t fsm[];
+                                                                        uint32_t* __restrict__ bits,
+                                                                        uint32_t* __restrict__ seg_info, uint64_t NS,
+                                                                        uint64_t spw) {
+  extern __shared__ __align__(128) uint32_t fsm[];
+  __shared__ __align__(8) uint64_t bars[kFastWarps][kStages];
+  __shared__ uint64_t sref[kFastWarps][kStages];
+  __shared__ uint32_t sw[kFastWarps][kStages];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kFastWarps + wid;
   const uint64_t s_begin = gw * spw;
   if (s_begin >= NS) return;
   const uint64_t s_end = min(NS, s_begin + spw);
   uint32_t* buf = fsm + wid * (kStages * kBufU32);
+  if (KIND != FAST_UNCOMPR && lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&bars[wid][k], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
 
-  auto meta = [&](uint64_t s, uint32_t& w, uint64_t& off, uint64_t& ref) {
+  auto issue = [&](uint64_t s, int stage) {
+    if (KIND == FAST_UNCOMPR || s >= s_end || lane != 0) return;
+    uint32_t w;
+    uint64_t off, ref = 0;
     if constexpr (KIND == FAST_STATIC) {
       w = c.w;
       off = s * 8 * (uint64_t)w;
-      ref = 0;
     } else {
       const uint64_t b = (s << 9) >> c.log2B;
-      const uint64_t piece = s & ((c.B >> 9) - 1);
       const uint32_t cw0 = __ldg(c.cw + b);
       w = __ldg(c.cw + b + 1) - cw0;
-      off = (uint64_t)cw0 * (c.B >> 6) + piece * 8 * (uint64_t)w;
-      ref = c.ref ? __ldg(c.ref + b) : 0;
+      off = (uint64_t)cw0 * (c.B >> 6) + (s & ((c.B >> 9) - 1)) * 8 * (uint64_t)w;
+      if (c.ref) ref = __ldg(c.ref + b);
     }
-  };
-  auto issue = [&](uint64_t s, int stage) {
-    if (KIND != FAST_UNCOMPR && s < s_end) {  // (UNCOMPR reads global memory directly)
-      uint32_t w;
-      uint64_t off, ref;
-      meta(s, w, off, ref);
-      const uint4* src = reinterpret_cast<const uint4*>(c.payload + off);
-      uint4* dst = reinterpret_cast<uint4*>(buf + stage * kBufU32);
-      const uint32_t chunks = w > 64 ? 0 : 4 * w;  // 64*w bytes in 16-byte chunks
-      for (uint32_t q = lane; q < chunks; q += 32) cp_async16(dst + q, src + q);
-    }
-    cp_async_commit();
+    if (w > 64) w = 65;  // corrupt width: decoded as no match (dispatch default)
+    sw[wid][stage] = w;
+    sref[wid][stage] = ref;
+    const uint32_t bytes = w <= 64 ? 64 * w : 0;
+    mbar_arrive_tx(&bars[wid][stage], bytes);
+    if (bytes) bulk_g2s(buf + stage * kBufU32, c.payload + off, bytes, &bars[wid][stage]);
   };
 
-  issue(s_begin, 0);
-  issue(s_begin + 1, 1);
+  for (int k = 0; k < kStages - 1; ++k) issue(s_begin + k, k);
   int stage = 0;
+  uint32_t phase = 0;
   for (uint64_t s = s_begin; s < s_end; ++s) {
-    issue(s + 2, (stage + 2) % kStages);
-    cp_async_wait<2>();
-    __syncwarp();
+    issue(s + kStages - 1, (stage + kStages - 1) % kStages);
     uint32_t my;
     if constexpr (KIND == FAST_UNCOMPR) {
       my = seg_uncompr(c.payload + s * kSegRows, pred, lane);
     } else {
-      uint32_t w;
-      uint64_t off, ref;
-      meta(s, w, off, ref);
-      my = seg_dispatch(w, buf + stage * kBufU32, pred, ref, lane);
+      mbar_wait(&bars[wid][stage], phase);
+      my = seg_dispatch(sw[wid][stage], buf + stage * kBufU32, pred, sref[wid][stage], lane);
     }
     __syncwarp();
     if (lane < kSegWords) bits[s * kSegWords + lane] = my;
-    const uint32_t cnt = (uint32_t)warp_sum(__popc(my));
-    const uint32_t last = (uint32_t)warp_max(my ? lane * 32 + 32 - __clz(my) : 0u);
+    const uint32_t cnt = __reduce_add_sync(kFull, __popc(my));
+    const uint32_t last = __reduce_max_sync(kFull, my ? lane * 32 + 32 - __clz(my) : 0u);
     if (lane == 0) seg_info[s] = cnt | (last << 16);
-    stage = (stage + 1) % kStages;
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
   }
-  cp_async_wait<0>();
 }
 
 }  // namespace ms
