@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--n-log2", type=int, default=32, help="rows of c5 (default 2^32, the config's size)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--pos-fmt", default="delta_bp:512", help="(experiments) positions format, e.g. uncompr")
+    ap.add_argument("--proj-fmt", default="for_bp:512", help="(experiments) projected column format")
     return ap.parse_args()
 
 
@@ -200,10 +202,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
 
+    def parse_fmt(spec):
+        name, _, arg = spec.partition(":")
+        return getattr(ms, name)(int(arg)) if arg else getattr(ms, name)()
+
+    pos_fmt, proj_fmt = parse_fmt(args.pos_fmt), parse_fmt(args.proj_fmt)
+
     def step():
-        pos = ms.select(X, ms.LT, SEL_C5, row_offset=start, out_fmt=ms.delta_bp(512))
+        pos = ms.select(X, ms.LT, SEL_C5, row_offset=start, out_fmt=pos_fmt)
         counts = D.allgather_counts(pos.n, dev) if world > 1 else [pos.n]
-        yp = ms.project(Y, pos, start, ms.for_bp(512))
+        yp = ms.project(Y, pos, start, proj_fmt)
         s = ms.agg_sum(yp)
         if world > 1:
             D.allreduce_u64_sum(s)

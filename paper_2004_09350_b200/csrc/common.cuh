@@ -152,6 +152,46 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, uint64_t t, 
   return excl;
 }
 
+// Split look-back for software-pipelined items: publish the aggregate early,
+// resolve the exclusive prefix later (by then the predecessors are done).
+__device__ __forceinline__ void lookback_publish(uint64_t* status, uint64_t t, uint64_t agg) {
+  if ((threadIdx.x & 31) == 0) st_volatile(&status[t], (t == 0 ? kFlagP : kFlagA) | agg);
+}
+__device__ __forceinline__ uint64_t lookback_resolve(uint64_t* status, uint64_t t, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) return 0;
+  uint64_t excl = 0;
+  int64_t base = (int64_t)t - 1;
+  while (true) {
+    const int64_t idx = base - lane;
+    uint64_t s = kFlagP;
+    if (idx >= 0) {
+      int spins = 0;
+      while (((s = ld_volatile(&status[idx])) >> 62) == 0) {
+        if (++spins > 8) __nanosleep(64);
+      }
+    }
+    const unsigned pmask = __ballot_sync(kFull, (s >> 62) == 2);
+    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
+    uint64_t v = (lane <= first_p) ? (s & kValMask) : 0;
+    excl += warp_sum(v);
+    if (pmask) break;
+    base -= 32;
+  }
+  if (lane == 0) st_volatile(&status[t], kFlagP | ((excl + agg) & kValMask));
+  return excl;
+}
+
+// floor(x / w) for x < 2^20, 1 <= w <= 64, given magic = 0xffffffff / w + 1
+// (computed once per block): a multiply-high plus one correction step
+__device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, uint32_t magic) {
+  if (w == 1) return x;
+  uint32_t q = __umulhi(x, magic);
+  if (q * w > x) --q;
+  if ((q + 1) * w <= x) ++q;
+  return q;
+}
+
 // ---------------------------------------------------------- random access
 // value at row r of a column (r < c.n). O(1) for UNCOMPR, STATIC_BP, DYN_BP,
 // FOR_BP (cw / ref headers, D-12); O(B) for DELTA_BP (prefix inside the

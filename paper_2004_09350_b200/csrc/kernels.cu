@@ -1,5 +1,6 @@
 // kernels.cu — select / scan / sum / RLE kernels and the launch wrappers.
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -647,16 +648,17 @@ static cudaError_t run_warp_encode(const Src& src, const PosEnc& e, uint64_t* st
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   if (!n_items) return cudaSuccess;
   auto k = warp_encode_kernel<Src>;
-  const size_t smem = (size_t)kEncWarps * e.G * 8;
+  const int warps = e.G >= 2048 ? 2 : 4;
+  const size_t smem = (size_t)warps * e.G * 8;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kEncWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)per_sm * num_sms();
-  const uint64_t need = (n_items + kEncWarps - 1) / kEncWarps;
+  const uint64_t need = (n_items + warps - 1) / warps;
   if (need < grid) grid = need;
   ProfScope prof_(name, s);
-  k<<<(int)grid, kEncWarps * 32, smem, s>>>(src, e, n_items, status, ticket, err);
+  k<<<(int)grid, warps * 32, smem, s>>>(src, e, n_items, status, ticket, err);
   return cudaGetLastError();
 }
 
@@ -665,9 +667,21 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
   return run_warp_encode(MaskSource{bits, NS, gstart, row_offset}, e, status, ticket, err, "pos_encode", s);
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {
-  return run_warp_encode(ProjectSource{pos, data, row_offset}, e, status, ticket, err, "project_warp", s);
+  // tuning knobs (defaults measured on B200; env overrides are for experiments)
+  const int batch = env_int("MS_GATHER_BATCH", 4);
+  const uint32_t pf = (uint32_t)env_int("MS_GATHER_PREFETCH", 1);
+  if (batch >= 16) return run_warp_encode(ProjectSource<16>{pos, data, row_offset, pf}, e, status, ticket, err,
+                                          "project_warp", s);
+  if (batch >= 8) return run_warp_encode(ProjectSource<8>{pos, data, row_offset, pf}, e, status, ticket, err,
+                                         "project_warp", s);
+  return run_warp_encode(ProjectSource<4>{pos, data, row_offset, pf}, e, status, ticket, err, "project_warp", s);
 }
 
 }  // namespace ms

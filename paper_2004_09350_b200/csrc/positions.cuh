@@ -78,10 +78,12 @@ struct MaskSource {
 // headers (cw, ref) of the data window are loaded once per warp (lane j ->
 // block b_lo + j) and broadcast by shuffles; each lane then has its 16
 // payload loads in flight at once.
+template <int BATCH>
 struct ProjectSource {
   ColView pos;
   ColView data;
   uint64_t row_offset;
+  uint32_t prefetch;  // bulk-prefetch the data window into L2 before gathering
   __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, uint64_t* P, uint32_t lane,
                                        uint32_t* err) const {
     // ---- positions
@@ -125,10 +127,21 @@ struct ProjectSource {
         h_last = (lane == 31 && bj <= data.nb) ? __ldg(data.cw + bj) : 0u;
       }
       const uint32_t h_cw1 = lane == 31 ? h_last : h_cw_next;
-      for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * 8) {
-        uint64_t v[8];
+      if (window && prefetch) {  // one bulk L2 prefetch of the whole payload window
+        const uint32_t c_lo = __shfl_sync(kFull, h_cw, 0);
+        const uint32_t nblk = (uint32_t)((phi >> data.log2B) - b_lo) + 1;
+        const uint32_t c_hi = __shfl_sync(kFull, h_cw1, (nblk - 1) & 31);
+        const uint64_t bytes = (uint64_t)(c_hi - c_lo) * (data.B / 8);
+        if (lane == 0 && bytes >= 16) {
+          const uint64_t* a = data.payload + (uint64_t)c_lo * (data.B / 64);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"((uint32_t)(bytes & ~15ull))
+                       : "memory");
+        }
+      }
+      for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * BATCH) {
+        uint64_t v[BATCH];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
           const uint64_t p = i < cnt ? P[i] : row_offset;
           const bool ok = p >= row_offset && p - row_offset < data.n;
@@ -157,7 +170,7 @@ struct ProjectSource {
           v[q] = rf + unpack_at(data.payload, (uint64_t)cw0 * data.B + (r & (data.B - 1)) * (uint64_t)w, w);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
           if (i < cnt) P[i] = v[q];
         }
@@ -175,12 +188,85 @@ struct ProjectSource {
   }
 };
 
-// Output-side buffer layer, one warp per item (G output rows). Dynamic shared
-// memory: warps x G uint64. The Source fills P[0..cnt) with the item's values.
-constexpr int kEncWarps = 4;
+// Output-side buffer layer, one warp per item (G output rows): the Source fills
+// the item's values into the warp's shared-memory tile (the paper's L1-resident
+// output buffer), the block width is published as a look-back aggregate, the
+// exclusive prefix resolved, and the block packed into whole words. (A
+// two-tile software pipeline that defers the look-back was measured slower:
+// it halves occupancy, and these kernels are latency-bound.)
+// Dynamic shared memory: warps x G uint64.
 template <class Src>
-__global__ void __launch_bounds__(kEncWarps * 32) warp_encode_kernel(Src src, PosEnc e, uint64_t n_items,
-                                                                     uint64_t* status, uint32_t* ticket, uint32_t* err) {
+__device__ __forceinline__ void encode_finish(const PosEnc& e, uint32_t item, uint64_t* P, uint32_t cnt,
+                                              uint32_t w, uint64_t rmin, uint64_t* status, uint32_t* err,
+                                              uint32_t lane) {
+  const bool is_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  const uint64_t r0 = (uint64_t)item * e.G;
+  if (!is_block) {
+    if (e.format == MS_UNCOMPR) {
+      for (uint32_t i = lane; i < cnt; i += 32) e.payload[r0 + i] = P[i];
+    } else if (e.format == MS_RLE) {
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        e.payload[2 * (r0 + i)] = P[i];
+        e.payload[2 * (r0 + i) + 1] = 1;
+      }
+    } else {  // STATIC_BP: item = ranks [512k, 512k+cnt) at bit 512k*w (word aligned)
+      const uint32_t ws = e.w;
+      const uint64_t mask = low_mask(ws);
+      const uint64_t wbase = (uint64_t)item * 8 * ws;
+      const uint32_t nwords = (uint32_t)(((uint64_t)cnt * ws + 63) / 64);
+      const uint32_t magic = 0xffffffffu / ws + 1u;
+      for (uint32_t m = lane; m < nwords; m += 32) {
+        const uint32_t bit0 = m * 64;
+        uint32_t j = div_small(bit0, ws, magic);
+        const uint32_t sft = bit0 - j * ws;
+        uint64_t acc = (P[j] & mask) >> sft;
+        for (++j; j < cnt; ++j) {
+          const uint32_t jb = j * ws;
+          if (jb >= bit0 + 64) break;
+          acc |= (P[j] & mask) << (jb - bit0);
+        }
+        e.payload[wbase + m] = acc;
+      }
+    }
+    return;
+  }
+  if (cnt < e.G) {  // final partial block -> uncompressed remainder
+    for (uint32_t i = lane; i < cnt; i += 32) e.rem[i] = P[i];
+    return;
+  }
+  const uint64_t E = lookback_resolve(status, item, w);
+  if (lane == 0) {
+    if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+    e.cw[item + 1] = (uint32_t)(E + w);
+    if (e.format == MS_DELTA_BP) e.ref[item] = P[0];
+    if (e.format == MS_FOR_BP) e.ref[item] = rmin;
+  }
+  if (!w) return;
+  const uint64_t wbase = E * (e.G >> 6);
+  const uint32_t nwords = (e.G >> 6) * w;
+  const uint32_t magic = 0xffffffffu / w + 1u;
+  for (uint32_t m = lane; m < nwords; m += 32) {
+    const uint32_t bit0 = m * 64;
+    uint32_t j = div_small(bit0, w, magic);
+    const uint32_t sft = bit0 - j * w;
+    auto code = [&](uint32_t i) -> uint64_t {
+      if (e.format == MS_DELTA_BP) return i ? P[i] - P[i - 1] : 0ull;
+      if (e.format == MS_FOR_BP) return P[i] - rmin;
+      return P[i];
+    };
+    uint64_t acc = code(j) >> sft;
+    for (++j; j < cnt; ++j) {
+      const uint32_t jb = j * w;
+      if (jb >= bit0 + 64) break;
+      acc |= code(j) << (jb - bit0);
+    }
+    e.payload[wbase + m] = acc;
+  }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(128) warp_encode_kernel(Src src, PosEnc e, uint64_t n_items, uint64_t* status,
+                                                          uint32_t* ticket, uint32_t* err) {
   extern __shared__ __align__(16) uint64_t enc_sm[];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t* P = enc_sm + (uint64_t)wid * e.G;
@@ -193,97 +279,39 @@ __global__ void __launch_bounds__(kEncWarps * 32) warp_encode_kernel(Src src, Po
     const uint64_t r0 = (uint64_t)item * e.G;
     const uint32_t cnt = (uint32_t)min((uint64_t)e.G, e.n_out - r0);
     src.load(item, r0, cnt, P, lane, err);
-    if (!is_block) {
-      if (e.format == MS_UNCOMPR) {
-        for (uint32_t i = lane; i < cnt; i += 32) e.payload[r0 + i] = P[i];
-      } else if (e.format == MS_RLE) {
+    uint32_t w = 0;
+    uint64_t rmin = 0;
+    if (is_block && cnt == e.G) {
+      uint64_t mx = 0;
+      if (e.format == MS_DELTA_BP) {
         for (uint32_t i = lane; i < cnt; i += 32) {
-          e.payload[2 * (r0 + i)] = P[i];
-          e.payload[2 * (r0 + i) + 1] = 1;
+          const uint64_t d = i ? P[i] - P[i - 1] : 0ull;
+          mx = d > mx ? d : mx;
         }
-      } else {  // STATIC_BP: item = ranks [512k, 512k+cnt) at bit 512k*w (word aligned)
-        const uint32_t w = e.w;
-        const uint64_t mask = low_mask(w);
-        const uint64_t wbase = (uint64_t)item * 8 * w;
-        const uint32_t nwords = (uint32_t)(((uint64_t)cnt * w + 63) / 64);
-        for (uint32_t m = lane; m < nwords; m += 32) {
-          const uint64_t bit0 = (uint64_t)m * 64;
-          uint32_t j = (uint32_t)(bit0 / w);
-          const uint32_t sft = (uint32_t)(bit0 - (uint64_t)j * w);
-          uint64_t acc = (P[j] & mask) >> sft;
-          for (++j; j < cnt; ++j) {
-            const uint64_t jb = (uint64_t)j * w;
-            if (jb >= bit0 + 64) break;
-            acc |= (P[j] & mask) << (jb - bit0);
-          }
-          e.payload[wbase + m] = acc;
+        mx = warp_max(mx);
+      } else {  // FOR: ebw(max - min); DYN: ebw(max) (values need not be sorted: project)
+        uint64_t lo = ~0ull, hi = 0;
+        for (uint32_t i = lane; i < cnt; i += 32) {
+          lo = P[i] < lo ? P[i] : lo;
+          hi = P[i] > hi ? P[i] : hi;
         }
-      }
-      __syncwarp();
-      continue;
-    }
-    if (cnt < e.G) {  // final partial block -> uncompressed remainder
-      for (uint32_t i = lane; i < cnt; i += 32) e.rem[i] = P[i];
-      __syncwarp();
-      continue;
-    }
-    // ---- block width
-    uint64_t mx = 0, rmin = 0;
-    if (e.format == MS_DELTA_BP) {
-      for (uint32_t i = lane; i < cnt; i += 32) {
-        const uint64_t d = i ? P[i] - P[i - 1] : 0ull;
-        mx = d > mx ? d : mx;
-      }
-      mx = warp_max(mx);
-    } else {  // FOR: ebw(max - min); DYN: ebw(max) (values need not be sorted: project)
-      uint64_t lo = ~0ull, hi = 0;
-      for (uint32_t i = lane; i < cnt; i += 32) {
-        lo = P[i] < lo ? P[i] : lo;
-        hi = P[i] > hi ? P[i] : hi;
-      }
-      hi = warp_max(hi);
-      if (e.format == MS_FOR_BP) {
+        hi = warp_max(hi);
+        if (e.format == MS_FOR_BP) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const uint64_t t = __shfl_xor_sync(kFull, lo, o);
-          lo = t < lo ? t : lo;
+          for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t t = __shfl_xor_sync(kFull, lo, o);
+            lo = t < lo ? t : lo;
+          }
+          mx = hi - lo;
+          rmin = lo;
+        } else {
+          mx = hi;
         }
-        mx = hi - lo;
-        rmin = lo;
-      } else {
-        mx = hi;
       }
+      w = ebw64(mx);
+      lookback_publish(status, item, w);
     }
-    const uint32_t w = ebw64(mx);
-    const uint64_t E = lookback_warp(status, item, w);
-    if (lane == 0) {
-      if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
-      e.cw[item + 1] = (uint32_t)(E + w);
-      if (e.format == MS_DELTA_BP) e.ref[item] = P[0];
-      if (e.format == MS_FOR_BP) e.ref[item] = rmin;
-    }
-    if (w) {
-      const uint64_t wbase = E * (e.G >> 6);
-      const uint32_t nwords = (e.G >> 6) * w;
-      const uint64_t rf = rmin;
-      for (uint32_t m = lane; m < nwords; m += 32) {
-        const uint64_t bit0 = (uint64_t)m * 64;
-        uint32_t j = (uint32_t)(bit0 / w);
-        const uint32_t sft = (uint32_t)(bit0 - (uint64_t)j * w);
-        auto code = [&](uint32_t i) -> uint64_t {
-          if (e.format == MS_DELTA_BP) return i ? P[i] - P[i - 1] : 0ull;
-          if (e.format == MS_FOR_BP) return P[i] - rf;
-          return P[i];
-        };
-        uint64_t acc = code(j) >> sft;
-        for (++j; j < cnt; ++j) {
-          const uint64_t jb = (uint64_t)j * w;
-          if (jb >= bit0 + 64) break;
-          acc |= code(j) << (jb - bit0);
-        }
-        e.payload[wbase + m] = acc;
-      }
-    }
+    encode_finish<Src>(e, item, P, cnt, w, rmin, status, err, lane);
     __syncwarp();
   }
 }

@@ -213,3 +213,31 @@ def test_host_roundtrip(rng):
     g = ms.Column.from_host(ms.for_bp(512), oc.n, oc.payload, oc.cw, oc.ref, oc.rem)
     assert_same_image(g, oc, "from_host")
     assert np.array_equal(ms.to_u64_numpy(ms.decompress(g)), v)
+
+
+def test_select_dense_and_sparse(rng):
+    """Width-1 deltas (every row selected), single matches, matches only in the
+    remainder, and empty results, through every output format."""
+    ms = get_ms()
+    outs = [ms.delta_bp(512), ms.delta_bp(128), ms.delta_bp(2048), ms.for_bp(512), ms.dyn_bp(1024),
+            ms.uncompr(), ms.static_bp(0), ms.rle()]
+    cases = []
+    n = 100_003
+    z = np.zeros(n, np.uint64)
+    cases.append((z, ms.GE, 0, 0))                       # all rows
+    one = z.copy(); one[77_777] = 5
+    cases.append((one, ms.EQ, 5, 0))                      # a single match
+    tail = z.copy(); tail[-3:] = 9
+    cases.append((tail, ms.EQ, 9, 0))                     # matches only in the final rows
+    cases.append((z, ms.EQ, 1, 0))                        # nothing
+    sparse = rng.integers(0, 1 << 20, n).astype(np.uint64)
+    cases.append((sparse, ms.LT, 1 << 8, 0))             # ~0.02% selectivity
+    for v, op, a, b in cases:
+        for fi in (ms.dyn_bp(512), ms.static_bp(0), ms.uncompr()):
+            gi = ms.compress(to_torch(v), fi)
+            oi = O.encode(v, *oracle_fmt(fi))
+            for fo in outs:
+                gs = ms.select(gi, op, a, b, row_offset=3, out_fmt=fo)
+                os_ = O.select(oi, oracle_op(op), a, b, row_offset=3, out_fmt=oracle_fmt(fo)[0],
+                               out_width=fo.bit_width, out_block=fo.block_size)
+                assert_same_image(gs, os_, f"select dense/sparse {fi} {op} {a} -> {fo}")
