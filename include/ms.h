@@ -74,12 +74,18 @@ typedef enum {
 
 /* Column descriptor {format, bit width, block size} (BASELINE.json north_star).
  * bit_width: STATIC_BP 1..64; 0 on an output spec = auto = max(1, ebw(max)).
- * block_size: DYN/FOR/DELTA 128, 256, 512, 1024 or 2048; ignored otherwise. */
+ * block_size: DYN/FOR/DELTA 128, 256, 512, 1024 or 2048; ignored otherwise.
+ * max_width: block formats: the largest block width of the column if known
+ *   (1..64), 0 = unknown. Not part of the image; a sizing hint that libms
+ *   producers fill in and scans use to pick narrower staging buffers. An
+ *   understated hint never causes an out-of-bounds access: blocks that do not
+ *   fit the chosen staging slot are reported as MS_E_CORRUPT. Ignored on
+ *   output specs. */
 typedef struct {
   int32_t format;
   uint32_t bit_width;
   uint32_t block_size;
-  uint32_t _reserved;
+  uint32_t max_width;
 } ms_fmt;
 
 /* A column: compressed main part + uncompressed remainder + metadata.

@@ -151,6 +151,7 @@ ColView view_of(const ms_column* c) {
   ColView v{};
   v.format = c->fmt.format;
   v.w = c->fmt.bit_width;
+  v.maxw = c->fmt.format == MS_STATIC_BP ? c->fmt.bit_width : (c->fmt.max_width <= 64 ? c->fmt.max_width : 0);
   v.B = is_block(c->fmt.format) ? c->fmt.block_size : 1;
   v.log2B = log2u(v.B);
   v.n = c->n;
@@ -196,6 +197,7 @@ ms_status alloc_column(const Ctx& ctx, ms_column* out, const ms_fmt& fmt, uint64
                        uint64_t n_runs) {
   std::memset(out, 0, sizeof(*out));
   out->fmt = fmt;
+  out->fmt.max_width = 0;
   out->n = n;
   uint64_t nb = 0, nrem = 0;
   if (is_block(fmt.format)) {
@@ -282,19 +284,37 @@ ms_status readback(const Ctx& ctx, const uint64_t* dev, uint64_t* host, size_t c
   return MS_OK;
 }
 
-// finish a block-format output: read cw[nb] and the error word
+// finish an output: read the error word and, for block formats, cw[nb] and
+// the largest block width (the max_width hint of the descriptor)
 ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev) {
   uint64_t h[2] = {0, 0};
+  uint32_t maxw = 0;
+  uint32_t* maxw_dev = nullptr;
+  if (is_block(out->fmt.format) && out->n_blocks) {
+    maxw_dev = (uint32_t*)ctx.alloc(4);
+    if (!maxw_dev) return MS_E_NOMEM;
+    cudaError_t e = cudaMemsetAsync(maxw_dev, 0, 4, ctx.s);
+    if (e == cudaSuccess) e = launch_max_width(out->cw, out->n_blocks, maxw_dev, ctx.s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&maxw, maxw_dev, 4, cudaMemcpyDeviceToHost, ctx.s);
+    if (e != cudaSuccess) {
+      ctx.free(maxw_dev);
+      return cuda_status(e);
+    }
+  }
   MS_TRY_CUDA(cudaMemcpyAsync(&h[0], err_dev, 4, cudaMemcpyDeviceToHost, ctx.s));
   if (is_block(out->fmt.format))
     MS_TRY_CUDA(cudaMemcpyAsync(&h[1], out->cw + out->n_blocks, 4, cudaMemcpyDeviceToHost, ctx.s));
   MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  ctx.free(maxw_dev);
   MS_TRY_CUDA(cudaGetLastError());
   const ms_status st = status_from_bits((uint32_t)h[0]);
   if (st != MS_OK) return st;
   if (is_block(out->fmt.format)) {
     if (out->n_blocks == 0) h[1] = 0;
     out->payload_words = (uint32_t)h[1] * (uint64_t)(out->fmt.block_size / 64);
+    out->fmt.max_width = maxw;
+  } else {
+    out->fmt.max_width = 0;
   }
   return MS_OK;
 }
@@ -517,6 +537,7 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
   if (same_fmt(in->fmt, fmt)) {  // identity morph: byte-identical
     MS_TRY(alloc_column(ctx, out, in->fmt, n, in->payload_words, in->n_runs));
     out->payload_words = in->payload_words;
+    out->fmt.max_width = in->fmt.max_width;
     if (in->payload_words)
       MS_TRY_CUDA(cudaMemcpyAsync(out->payload, in->payload, 8 * in->payload_words, cudaMemcpyDeviceToDevice, ctx.s));
     if (is_block(fmt.format)) {
@@ -584,7 +605,7 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   ColView src = view_of(in);
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
   uint64_t* seg_off = sc.at<uint64_t>(o_off);
-  MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, ctx.s));
+  MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, err, ctx.s));
   MS_TRY_CUDA(launch_seg_scan(sc.at<uint32_t>(o_seg), sc.at<uint32_t>(o_bits), NS, row_offset, G, seg_off,
                               sc.at<uint64_t>(o_gs), sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1),
                               sc.at<uint32_t>(o_tk1), ctx.s));
@@ -786,6 +807,14 @@ ms_status ms_column_to_device(const ms_ctx* ctx_, const ms_column* h, ms_column*
   Ctx ctx(ctx_);
   MS_TRY(alloc_column(ctx, out, h->fmt, h->n, h->payload_words, h->n_runs));
   out->payload_words = h->payload_words;
+  if (is_block(h->fmt.format)) {  // the max_width hint, from the host copy of cw
+    uint32_t mw = 0;
+    for (uint64_t b = 0; b < h->n_blocks; ++b) {
+      const uint32_t w = h->cw[b + 1] - h->cw[b];
+      mw = w > mw ? w : mw;
+    }
+    out->fmt.max_width = mw <= 64 ? mw : 0;
+  }
   auto cp = [&](void* d, const void* s, uint64_t bytes) {
     return bytes ? cudaMemcpyAsync(d, s, bytes, cudaMemcpyHostToDevice, ctx.s) : cudaSuccess;
   };

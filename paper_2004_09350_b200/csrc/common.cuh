@@ -35,6 +35,7 @@ __host__ __device__ constexpr uint32_t err_bit(int s) { return 1u << s; }
 struct ColView {
   int32_t format;
   uint32_t w;          // STATIC_BP width
+  uint32_t maxw;       // block formats: largest block width hint (0 = unknown)
   uint32_t B;          // block size (block formats)
   uint32_t log2B;
   uint64_t n, nb, nrem, nruns;

@@ -117,6 +117,11 @@ static uint64_t n_items_hint(const OutView& o) {
   return (o.n + kChunk - 1) / kChunk;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // ----------------------------------------------------------------- engine
 cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s) {
   auto k = engine_kernel<ColSource>;
@@ -201,8 +206,26 @@ __global__ void __launch_bounds__(kThreads) select_generic_kernel(ColView c, Pre
   }
 }
 
+__global__ void max_width_kernel(const uint32_t* cw, uint64_t nb, uint32_t* out) {
+  uint32_t m = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride)
+    m = max(m, cw[b + 1] - cw[b]);
+  m = __reduce_max_sync(kFull, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cudaStream_t s) {
+  if (!nb) return cudaSuccess;
+  uint64_t grid = (nb + 255) / 256;
+  if (grid > (uint64_t)num_sms() * 8) grid = num_sms() * 8;
+  ProfScope prof_("max_width", s);
+  max_width_kernel<<<(int)grid, 256, 0, s>>>(cw, nb, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
-                          cudaStream_t s) {
+                          uint32_t* err, cudaStream_t s) {
   if (NS == 0) return cudaSuccess;
   // fast path: UNCOMPR, STATIC_BP, DYN_BP / FOR_BP with B >= 512, on full 512-row segments
   int kind = -1;
@@ -215,22 +238,36 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
   }
   if (kind >= 0 && ns_fast) {
     FastPred fp{p.lo, p.span, p.neg, (uint32_t)p.is_bitmap, p.bitmap, p.bitmap_bits};
-    const size_t smem = (size_t)kFastWarps * kStages * kBufU32 * 4;
-    auto pick = [&](auto k) {
+    auto pick = [&](auto k, int stages, int warps_per_cta, int bufu32 = kPairBufWide) {
+      const size_t smem = (size_t)warps_per_cta * stages * bufu32 * 4;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFastWarps * 32, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps_per_cta * 32, smem);
       if (per_sm < 1) per_sm = 1;
-      const uint64_t warps = (uint64_t)per_sm * num_sms() * kFastWarps;
-      const uint64_t spw = (ns_fast + warps - 1) / warps;
+      const uint64_t warps = (uint64_t)per_sm * num_sms() * warps_per_cta;
+      uint64_t spw = (ns_fast + warps - 1) / warps;
+      spw += spw & 1;  // whole segment pairs per warp
       const uint64_t used = (ns_fast + spw - 1) / spw;
-      const int grid = (int)((used + kFastWarps - 1) / kFastWarps);
+      const int grid = (int)((used + warps_per_cta - 1) / warps_per_cta);
       ProfScope prof_("select_fast", s);
-      k<<<grid, kFastWarps * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw);
+      k<<<grid, warps_per_cta * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw, err);
     };
-    if (kind == FAST_UNCOMPR) pick(select_fast_kernel<FAST_UNCOMPR>);
-    else if (kind == FAST_STATIC) pick(select_fast_kernel<FAST_STATIC>);
-    else pick(select_fast_kernel<FAST_BLOCK>);
+    // variants (stages, warps/CTA, min CTAs/SM); default measured on B200, env override for experiments
+    const int v = env_int("MS_SELECT_VARIANT", 0);
+    // narrow staging slots (2 x 2 KiB per pair) when every block is <= 32 bits wide
+    const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
+#define MS_PICK(K)                                                             \
+  do {                                                                         \
+    if (v == 1) pick(select_fast_kernel<K, 3, 4, 2>, 3, 4);                    \
+    else if (v == 2) pick(select_fast_kernel<K, 2, 8, 1>, 2, 8);               \
+    else if (v == 3) pick(select_fast_kernel<K, 3, 4, 4, kPairBufNarrow>, 3, 4, kPairBufNarrow); \
+    else if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow); \
+    else pick(select_fast_kernel<K, 2, 4, 3>, 2, 4);                           \
+  } while (0)
+    if (kind == FAST_UNCOMPR) MS_PICK(FAST_UNCOMPR);
+    else if (kind == FAST_STATIC) MS_PICK(FAST_STATIC);
+    else MS_PICK(FAST_BLOCK);
+#undef MS_PICK
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -667,10 +704,6 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
   return run_warp_encode(MaskSource{bits, NS, gstart, row_offset}, e, status, ticket, err, "pos_encode", s);
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
 
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {

@@ -46,7 +46,7 @@ cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64
 
 // select core: bit mask (16 words per 512-row segment) + seg_info (count | last << 16)
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
-                          cudaStream_t s);
+                          uint32_t* err, cudaStream_t s);
 // exclusive scan of per-segment counts -> seg_off[0..NS], start_seg[] per output item, 1 + max position
 // ... and, for every output item of G ranks starting in a segment, the item's first position
 cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint64_t NS, uint64_t row_offset,
@@ -88,5 +88,7 @@ cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t
                                unsigned long long* sums, uint32_t* err, cudaStream_t s);
 
 int num_sms();
+// largest block width max(cw[b+1] - cw[b]) into *out (zero-initialised)
+cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cudaStream_t s);
 
 }  // namespace ms

@@ -11,9 +11,7 @@
 
 namespace ms {
 
-constexpr int kStages = 3;
 constexpr int kBufU32 = 1024 + 8;        // 4 KiB (512 rows x 64 bit) + padding for look-ahead reads
-constexpr int kFastWarps = 8;            // warps per CTA
 
 enum : int { FAST_UNCOMPR = 0, FAST_STATIC = 1, FAST_BLOCK = 2 };
 
@@ -59,128 +57,6 @@ __device__ __forceinline__ void code_interval(uint64_t lo, uint64_t span, uint32
   }
 }
 
-// Decode + predicate one 512-row segment of width W from shared memory (u32
-// words, LSB-first). Lane l handles rows l + 32k; word index l*W/32 + k*W and
-// shift l*W mod 32 are per-lane constants. Lane k (< 16) receives mask word k.
-template <int W>
-__device__ __forceinline__ uint32_t seg_range32(const uint32_t* __restrict__ s, uint32_t a, uint32_t sp,
-                                                uint32_t neg, uint32_t lane) {
-  uint32_t my = 0;
-  if constexpr (W == 0) {
-    const bool keep = ((0u - a) <= sp) != (neg != 0);
-    return lane < kSegWords ? (keep ? 0xffffffffu : 0u) : 0u;
-  } else {
-    constexpr uint32_t mask = W >= 32 ? 0xffffffffu : ((1u << (W & 31)) - 1);
-    const uint32_t bitl = lane * W;
-    const uint32_t* p = s + (bitl >> 5);
-    const uint32_t sh = bitl & 31;
-#pragma unroll
-    for (int k = 0; k < kSegWords; ++k) {
-      const uint32_t code = __funnelshift_r(p[k * W], p[k * W + 1], sh) & mask;
-      const bool keep = ((code - a) <= sp) != (neg != 0);
-      const uint32_t word = __ballot_sync(kFull, keep);
-      if (lane == (uint32_t)k) my = word;
-    }
-  }
-  return my;
-}
-
-template <int W>
-__device__ __forceinline__ uint32_t seg_range64(const uint32_t* __restrict__ s, uint64_t d, uint64_t sp,
-                                                uint32_t neg, uint32_t lane) {
-  uint32_t my = 0;
-  constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
-  const uint32_t bitl = lane * W;
-  const uint32_t* p = s + (bitl >> 5);
-  const uint32_t sh = bitl & 31;
-#pragma unroll
-  for (int k = 0; k < kSegWords; ++k) {
-    const uint32_t w0 = p[k * W], w1 = p[k * W + 1], w2 = p[k * W + 2];
-    const uint64_t code =
-        (((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh)) & mask;
-    const bool keep = ((code - d) <= sp) != (neg != 0);
-    const uint32_t word = __ballot_sync(kFull, keep);
-    if (lane == (uint32_t)k) my = word;
-  }
-  return my;
-}
-
-template <int W>
-__device__ __forceinline__ uint32_t seg_bitmap(const uint32_t* __restrict__ s, uint64_t ref, const uint64_t* bm,
-                                               uint64_t bits, uint32_t lane) {
-  uint32_t my = 0;
-  constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
-  const uint32_t bitl = lane * W;
-  const uint32_t* p = s + (bitl >> 5);
-  const uint32_t sh = bitl & 31;
-#pragma unroll 4
-  for (int k = 0; k < kSegWords; ++k) {
-    uint64_t code = 0;
-    if (W > 0) {
-      const uint32_t w0 = p[k * W], w1 = p[k * W + 1], w2 = W > 32 ? p[k * W + 2] : 0u;
-      code = (((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh)) & mask;
-    }
-    const uint64_t v = ref + code;
-    const bool keep = v < bits && ((__ldg(bm + (v >> 6)) >> (v & 63)) & 1ull);
-    const uint32_t word = __ballot_sync(kFull, keep);
-    if (lane == (uint32_t)k) my = word;
-  }
-  return my;
-}
-
-// runtime width -> compile-time width (one instantiation per width)
-template <int W>
-__device__ __forceinline__ uint32_t seg_one(const uint32_t* s, const FastPred& p, uint64_t ref, uint32_t lane) {
-  if (p.is_bitmap) return seg_bitmap<W>(s, ref, p.bitmap, p.bits, lane);
-  if constexpr (W <= 32) {
-    uint32_t a, sp, ng;
-    code_interval(p.lo, p.span, p.neg, ref, W, a, sp, ng);
-    return seg_range32<W>(s, a, sp, ng, lane);
-  } else {
-    return seg_range64<W>(s, p.lo - ref, p.span, p.neg, lane);
-  }
-}
-
-__device__ __forceinline__ uint32_t seg_dispatch(uint32_t w, const uint32_t* s, const FastPred& p, uint64_t ref,
-                                              uint32_t lane) {
-  switch (w) {
-#define MS_SEG_CASE(W) \
-  case W:              \
-    return seg_one<W>(s, p, ref, lane);
-    MS_SEG_CASE(0) MS_SEG_CASE(1) MS_SEG_CASE(2) MS_SEG_CASE(3) MS_SEG_CASE(4) MS_SEG_CASE(5) MS_SEG_CASE(6)
-    MS_SEG_CASE(7) MS_SEG_CASE(8) MS_SEG_CASE(9) MS_SEG_CASE(10) MS_SEG_CASE(11) MS_SEG_CASE(12)
-    MS_SEG_CASE(13) MS_SEG_CASE(14) MS_SEG_CASE(15) MS_SEG_CASE(16) MS_SEG_CASE(17) MS_SEG_CASE(18)
-    MS_SEG_CASE(19) MS_SEG_CASE(20) MS_SEG_CASE(21) MS_SEG_CASE(22) MS_SEG_CASE(23) MS_SEG_CASE(24)
-    MS_SEG_CASE(25) MS_SEG_CASE(26) MS_SEG_CASE(27) MS_SEG_CASE(28) MS_SEG_CASE(29) MS_SEG_CASE(30)
-    MS_SEG_CASE(31) MS_SEG_CASE(32) MS_SEG_CASE(33) MS_SEG_CASE(34) MS_SEG_CASE(35) MS_SEG_CASE(36)
-    MS_SEG_CASE(37) MS_SEG_CASE(38) MS_SEG_CASE(39) MS_SEG_CASE(40) MS_SEG_CASE(41) MS_SEG_CASE(42)
-    MS_SEG_CASE(43) MS_SEG_CASE(44) MS_SEG_CASE(45) MS_SEG_CASE(46) MS_SEG_CASE(47) MS_SEG_CASE(48)
-    MS_SEG_CASE(49) MS_SEG_CASE(50) MS_SEG_CASE(51) MS_SEG_CASE(52) MS_SEG_CASE(53) MS_SEG_CASE(54)
-    MS_SEG_CASE(55) MS_SEG_CASE(56) MS_SEG_CASE(57) MS_SEG_CASE(58) MS_SEG_CASE(59) MS_SEG_CASE(60)
-    MS_SEG_CASE(61) MS_SEG_CASE(62) MS_SEG_CASE(63) MS_SEG_CASE(64)
-#undef MS_SEG_CASE
-    default:
-      return 0;
-  }
-}
-
-// UNCOMPR segment: 16 coalesced 64-bit loads per lane, predicate on the values
-__device__ __forceinline__ uint32_t seg_uncompr(const uint64_t* __restrict__ v, const FastPred& p, uint32_t lane) {
-  uint64_t x[kSegWords];
-#pragma unroll
-  for (int k = 0; k < kSegWords; ++k) x[k] = __ldg(v + lane + 32 * k);
-  uint32_t my = 0;
-#pragma unroll
-  for (int k = 0; k < kSegWords; ++k) {
-    bool keep;
-    if (p.is_bitmap) keep = x[k] < p.bits && ((__ldg(p.bitmap + (x[k] >> 6)) >> (x[k] & 63)) & 1ull);
-    else keep = ((x[k] - p.lo) <= p.span) != (p.neg != 0);
-    const uint32_t word = __ballot_sync(kFull, keep);
-    if (lane == (uint32_t)k) my = word;
-  }
-  return my;
-}
-
 // ---- TMA bulk copy + mbarrier helpers (sm_90+; SASS UBLKCP / SYNCS)
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
@@ -213,36 +89,178 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Per-warp contiguous range of full 512-row segments [s_begin, s_end). Lane 0
-// streams each segment's packed payload (64*w bytes, 64-byte aligned) into a
-// per-warp ring of kStages shared-memory slots with one TMA bulk copy, tracked
-// by one mbarrier per slot; the width / reference of the segment travel with
-// the slot, so decoding needs no further global reads.
-template <int KIND>
-__global__ void __launch_bounds__(kFastWarps * 32, 2) select_fast_kernel(ColView c, FastPred pred,
-                                                                        uint32_t* __restrict__ bits,
-                                                                        uint32_t* __restrict__ seg_info, uint64_t NS,
-                                                                        uint64_t spw) {
+// ---- lane-consecutive core: lane l of a half-warp owns rows 32l .. 32l+31 of
+// a segment = exactly W consecutive 32-bit words at word offset l*W (aligned:
+// 32 rows x W bits = W words), loaded with the widest aligned shared-memory
+// vector loads, unpacked with compile-time shifts, the predicate applied and
+// the lane's mask word built directly (no ballot, no cross-lane routing).
+template <int W>
+__device__ __forceinline__ void load_words(const uint32_t* __restrict__ p, uint32_t (&r)[W + 1]) {
+  if constexpr (W % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
+      r[i] = v.x; r[i + 1] = v.y; r[i + 2] = v.z; r[i + 3] = v.w;
+    }
+  } else if constexpr (W % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < W; i += 2) {
+      const uint2 v = *reinterpret_cast<const uint2*>(p + i);
+      r[i] = v.x; r[i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; ++i) r[i] = p[i];
+  }
+  r[W] = 0;
+}
+
+template <int W>
+__device__ __forceinline__ uint64_t code_at(const uint32_t (&r)[W + 1], int i) {
+  constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
+  const int bit = i * W, q = bit >> 5, sh = bit & 31;
+  if (W <= 32) {
+    uint32_t c = (sh + W <= 32) ? (r[q] >> sh) : __funnelshift_r(r[q], r[q + 1], sh);
+    return (uint64_t)(c & (uint32_t)mask);
+  }
+  const uint32_t lo = __funnelshift_r(r[q], r[q + 1], sh);
+  const uint32_t hi = (q + 2 <= W) ? __funnelshift_r(r[q + 1], r[(q + 2) <= W ? q + 2 : W], sh) : (r[q + 1] >> sh);
+  return (((uint64_t)hi << 32) | lo) & mask;
+}
+
+// one lane's 32 rows: returns the mask word (bit i <=> row 32l + i matched)
+template <int W>
+__device__ __forceinline__ uint32_t lane_rows(const uint32_t* __restrict__ p, const FastPred& pr, uint64_t ref) {
+  if constexpr (W == 0) {
+    bool keep;
+    if (pr.is_bitmap) keep = ref < pr.bits && ((__ldg(pr.bitmap + (ref >> 6)) >> (ref & 63)) & 1ull);
+    else keep = ((ref - pr.lo) <= pr.span) != (pr.neg != 0);
+    return keep ? 0xffffffffu : 0u;
+  } else {
+    uint32_t r[W + 1];
+    load_words<W>(p, r);
+    uint32_t m = 0;
+    if (pr.is_bitmap) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint64_t v = ref + code_at<W>(r, i);
+        const bool keep = v < pr.bits && ((__ldg(pr.bitmap + (v >> 6)) >> (v & 63)) & 1ull);
+        m |= (keep ? 1u : 0u) << i;
+      }
+    } else if constexpr (W <= 32) {
+      uint32_t a, sp, ng;
+      code_interval(pr.lo, pr.span, pr.neg, ref, W, a, sp, ng);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t c = (uint32_t)code_at<W>(r, i);
+        const bool keep = ((c - a) <= sp) != (ng != 0);
+        m |= (keep ? 1u : 0u) << i;
+      }
+    } else {
+      const uint64_t d = pr.lo - ref;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const bool keep = ((code_at<W>(r, i) - d) <= pr.span) != (pr.neg != 0);
+        m |= (keep ? 1u : 0u) << i;
+      }
+    }
+    return m;
+  }
+}
+
+// W > 32: the same 32 rows in two halves of 16 rows (16*W bits each) so that at
+// most W/2 + 2 words are live in registers; the second half starts at the
+// compile-time bit offset 16*W.
+template <int W, int H>
+__device__ __forceinline__ uint32_t half_rows(const uint32_t* __restrict__ p, const FastPred& pr, uint64_t ref,
+                                              uint64_t d) {
+  constexpr int B0 = H * 16 * W;       // first bit of this half
+  constexpr int Q0 = B0 >> 5;          // first word
+  constexpr int NW = ((B0 & 31) + 16 * W + 31) / 32 + 1;
+  constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
+  uint32_t r[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) r[i] = (Q0 + i < W) ? p[Q0 + i] : 0u;
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int bit = (B0 & 31) + i * W, q = bit >> 5, sh = bit & 31;
+    const uint32_t lo = __funnelshift_r(r[q], r[q + 1], sh);
+    const uint32_t hi = __funnelshift_r(r[q + 1], r[q + 2 < NW ? q + 2 : NW - 1], sh);
+    const uint64_t code = (((uint64_t)hi << 32) | lo) & mask;
+    bool keep;
+    if (pr.is_bitmap) {
+      const uint64_t v = ref + code;
+      keep = v < pr.bits && ((__ldg(pr.bitmap + (v >> 6)) >> (v & 63)) & 1ull);
+    } else {
+      keep = ((code - d) <= pr.span) != (pr.neg != 0);
+    }
+    m |= (keep ? 1u : 0u) << (i + 16 * H);
+  }
+  return m;
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t lane_rows_wide(const uint32_t* __restrict__ p, const FastPred& pr,
+                                                   uint64_t ref) {
+  const uint64_t d = pr.lo - ref;
+  return half_rows<W, 0>(p, pr, ref, d) | half_rows<W, 1>(p, pr, ref, d);
+}
+
+__device__ __forceinline__ uint32_t lane_dispatch(uint32_t w, const uint32_t* p, const FastPred& pr, uint64_t ref) {
+  switch (w) {
+#define MS_LANE_CASE(W) \
+  case W:               \
+    return W <= 32 ? lane_rows<(W <= 32 ? W : 1)>(p, pr, ref) : lane_rows_wide<(W > 32 ? W : 33)>(p, pr, ref);
+    MS_LANE_CASE(0) MS_LANE_CASE(1) MS_LANE_CASE(2) MS_LANE_CASE(3) MS_LANE_CASE(4) MS_LANE_CASE(5)
+    MS_LANE_CASE(6) MS_LANE_CASE(7) MS_LANE_CASE(8) MS_LANE_CASE(9) MS_LANE_CASE(10) MS_LANE_CASE(11)
+    MS_LANE_CASE(12) MS_LANE_CASE(13) MS_LANE_CASE(14) MS_LANE_CASE(15) MS_LANE_CASE(16) MS_LANE_CASE(17)
+    MS_LANE_CASE(18) MS_LANE_CASE(19) MS_LANE_CASE(20) MS_LANE_CASE(21) MS_LANE_CASE(22) MS_LANE_CASE(23)
+    MS_LANE_CASE(24) MS_LANE_CASE(25) MS_LANE_CASE(26) MS_LANE_CASE(27) MS_LANE_CASE(28) MS_LANE_CASE(29)
+    MS_LANE_CASE(30) MS_LANE_CASE(31) MS_LANE_CASE(32) MS_LANE_CASE(33) MS_LANE_CASE(34) MS_LANE_CASE(35)
+    MS_LANE_CASE(36) MS_LANE_CASE(37) MS_LANE_CASE(38) MS_LANE_CASE(39) MS_LANE_CASE(40) MS_LANE_CASE(41)
+    MS_LANE_CASE(42) MS_LANE_CASE(43) MS_LANE_CASE(44) MS_LANE_CASE(45) MS_LANE_CASE(46) MS_LANE_CASE(47)
+    MS_LANE_CASE(48) MS_LANE_CASE(49) MS_LANE_CASE(50) MS_LANE_CASE(51) MS_LANE_CASE(52) MS_LANE_CASE(53)
+    MS_LANE_CASE(54) MS_LANE_CASE(55) MS_LANE_CASE(56) MS_LANE_CASE(57) MS_LANE_CASE(58) MS_LANE_CASE(59)
+    MS_LANE_CASE(60) MS_LANE_CASE(61) MS_LANE_CASE(62) MS_LANE_CASE(63) MS_LANE_CASE(64)
+#undef MS_LANE_CASE
+    default:
+      return 0;
+  }
+}
+
+// Per-warp contiguous range of full 512-row segments, taken two at a time
+// (half-warp h handles segment 2p+h). Lane 0 streams the pair's packed payload
+// (64*(wA+wB) bytes, contiguous, 64-byte aligned) into a per-warp ring of
+// kStages shared-memory slots with ONE TMA bulk copy tracked by one mbarrier;
+// widths / references travel with the slot.
+constexpr int kPairBufWide = 2048 + 16;   // two segments at up to 64 bits + padding
+constexpr int kPairBufNarrow = 1024 + 16; // two segments at up to 32 bits + padding
+template <int KIND, int kStages = 2, int kFastWarps = 4, int kMinBlocks = 3, int kPairBufU32 = kPairBufWide>
+__global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kernel(ColView c, FastPred pred,
+                                                                                 uint32_t* __restrict__ bits,
+                                                                                 uint32_t* __restrict__ seg_info,
+                                                                                 uint64_t NS, uint64_t spw,
+                                                                                 uint32_t* err) {
   extern __shared__ __align__(128) uint32_t fsm[];
   __shared__ __align__(8) uint64_t bars[kFastWarps][kStages];
-  __shared__ uint64_t sref[kFastWarps][kStages];
-  __shared__ uint32_t sw[kFastWarps][kStages];
+  __shared__ uint64_t sref[kFastWarps][kStages][2];
+  __shared__ uint32_t sw[kFastWarps][kStages][2];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t half = lane >> 4, hl = lane & 15;
   const uint64_t gw = (uint64_t)blockIdx.x * kFastWarps + wid;
-  const uint64_t s_begin = gw * spw;
+  const uint64_t s_begin = gw * spw;  // spw is even
   if (s_begin >= NS) return;
   const uint64_t s_end = min(NS, s_begin + spw);
-  uint32_t* buf = fsm + wid * (kStages * kBufU32);
+  uint32_t* buf = fsm + wid * (kStages * kPairBufU32);
   if (KIND != FAST_UNCOMPR && lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&bars[wid][k], 1);
     mbar_fence_init();
   }
   __syncwarp();
 
-  auto issue = [&](uint64_t s, int stage) {
-    if (KIND == FAST_UNCOMPR || s >= s_end || lane != 0) return;
-    uint32_t w;
-    uint64_t off, ref = 0;
+  auto meta = [&](uint64_t s, uint32_t& w, uint64_t& off, uint64_t& ref) {
+    ref = 0;
     if constexpr (KIND == FAST_STATIC) {
       w = c.w;
       off = s * 8 * (uint64_t)w;
@@ -253,31 +271,74 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) select_fast_kernel(ColView
       off = (uint64_t)cw0 * (c.B >> 6) + (s & ((c.B >> 9) - 1)) * 8 * (uint64_t)w;
       if (c.ref) ref = __ldg(c.ref + b);
     }
-    if (w > 64) w = 65;  // corrupt width: decoded as no match (dispatch default)
-    sw[wid][stage] = w;
-    sref[wid][stage] = ref;
-    const uint32_t bytes = w <= 64 ? 64 * w : 0;
+    if (w > 64) {  // corrupt width table
+      w = 65;
+      atomicOr(err, err_bit(MS_E_CORRUPT));
+    }
+  };
+  auto issue = [&](uint64_t s, int stage) {  // segments s, s+1
+    if (KIND == FAST_UNCOMPR || s >= s_end || lane != 0) return;
+    uint32_t wa, wb = 0;
+    uint64_t off, ra, rb = 0, offb;
+    meta(s, wa, off, ra);
+    if (s + 1 < s_end) meta(s + 1, wb, offb, rb);
+    sw[wid][stage][0] = wa;
+    sw[wid][stage][1] = wb;
+    sref[wid][stage][0] = ra;
+    sref[wid][stage][1] = rb;
+    uint32_t bytes = (wa <= 64 ? 64 * wa : 0) + (wb <= 64 ? 64 * wb : 0);
+    if (bytes > (kPairBufU32 - 16) * 4) {  // a width larger than the max_width hint: never overrun the slot
+      sw[wid][stage][0] = sw[wid][stage][1] = 65;
+      bytes = 0;
+      atomicOr(err, err_bit(MS_E_CORRUPT));
+    }
     mbar_arrive_tx(&bars[wid][stage], bytes);
-    if (bytes) bulk_g2s(buf + stage * kBufU32, c.payload + off, bytes, &bars[wid][stage]);
+    if (bytes) bulk_g2s(buf + stage * kPairBufU32, c.payload + off, bytes, &bars[wid][stage]);
   };
 
-  for (int k = 0; k < kStages - 1; ++k) issue(s_begin + k, k);
+  for (int k = 0; k < kStages - 1; ++k) issue(s_begin + 2 * k, k);
   int stage = 0;
   uint32_t phase = 0;
-  for (uint64_t s = s_begin; s < s_end; ++s) {
-    issue(s + kStages - 1, (stage + kStages - 1) % kStages);
-    uint32_t my;
+  for (uint64_t s = s_begin; s < s_end; s += 2) {
+    issue(s + 2 * (kStages - 1), (stage + kStages - 1) % kStages);
+    const uint64_t my_seg = s + half;
+    const bool valid = my_seg < s_end;
+    uint32_t m = 0;
     if constexpr (KIND == FAST_UNCOMPR) {
-      my = seg_uncompr(c.payload + s * kSegRows, pred, lane);
+      if (valid) {
+        const uint64_t* v = c.payload + my_seg * kSegRows + hl * 32;
+        uint64_t x[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(v + i));
+          x[i] = t.x; x[i + 1] = t.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          bool keep;
+          if (pred.is_bitmap) keep = x[i] < pred.bits && ((__ldg(pred.bitmap + (x[i] >> 6)) >> (x[i] & 63)) & 1ull);
+          else keep = ((x[i] - pred.lo) <= pred.span) != (pred.neg != 0);
+          m |= (keep ? 1u : 0u) << i;
+        }
+      }
     } else {
       mbar_wait(&bars[wid][stage], phase);
-      my = seg_dispatch(sw[wid][stage], buf + stage * kBufU32, pred, sref[wid][stage], lane);
+      const uint32_t wa = sw[wid][stage][0];
+      const uint32_t w = sw[wid][stage][half];
+      const uint64_t ref = sref[wid][stage][half];
+      const uint32_t* p = buf + stage * kPairBufU32 + (half ? 16 * wa : 0) + hl * w;
+      if (valid) m = lane_dispatch(w, p, pred, ref);
     }
     __syncwarp();
-    if (lane < kSegWords) bits[s * kSegWords + lane] = my;
-    const uint32_t cnt = __reduce_add_sync(kFull, __popc(my));
-    const uint32_t last = __reduce_max_sync(kFull, my ? lane * 32 + 32 - __clz(my) : 0u);
-    if (lane == 0) seg_info[s] = cnt | (last << 16);
+    if (valid) bits[my_seg * kSegWords + hl] = m;
+    uint32_t cnt = __popc(m);
+    uint32_t last = m ? hl * 32 + 32 - __clz(m) : 0u;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      cnt += __shfl_xor_sync(kFull, cnt, o);
+      last = max(last, __shfl_xor_sync(kFull, last, o));
+    }
+    if (valid && hl == 0) seg_info[my_seg] = cnt | (last << 16);
     if (++stage == kStages) {
       stage = 0;
       phase ^= 1u;

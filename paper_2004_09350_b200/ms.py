@@ -60,7 +60,7 @@ def rle() -> Fmt: return Fmt(RLE)
 
 class _Fmt(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("bit_width", ctypes.c_uint32), ("block_size", ctypes.c_uint32),
-                ("_reserved", ctypes.c_uint32)]
+                ("max_width", ctypes.c_uint32)]
 
 
 class _Column(ctypes.Structure):
@@ -183,6 +183,7 @@ class Column:
         f = self._c.fmt
         return Fmt(f.format, f.bit_width, f.block_size)
 
+    max_width = property(lambda self: int(self._c.fmt.max_width))  # sizing hint (0 = unknown)
     n = property(lambda self: int(self._c.n))
     n_blocks = property(lambda self: int(self._c.n_blocks))
     n_rem = property(lambda self: int(self._c.n_rem))

@@ -241,3 +241,31 @@ def test_select_dense_and_sparse(rng):
                 os_ = O.select(oi, oracle_op(op), a, b, row_offset=3, out_fmt=oracle_fmt(fo)[0],
                                out_width=fo.bit_width, out_block=fo.block_size)
                 assert_same_image(gs, os_, f"select dense/sparse {fi} {op} {a} -> {fo}")
+
+
+def test_max_width_hint(rng):
+    """The descriptor's max_width sizing hint is set by producers and a wrong
+    hint is caught instead of trusted (select falls back to MS_E_CORRUPT)."""
+    ms = get_ms()
+    v = rng.integers(0, 1 << 20, 10_000).astype(np.uint64)
+    v[5000] = (1 << 40) + 3
+    c = ms.compress(to_torch(v), ms.dyn_bp(512))
+    w = np.diff(O.encode(v, O.DYN_BP, 0, 512).cw.astype(np.int64))
+    assert c.max_width == int(w.max()) == 41
+    narrow = ms.compress(to_torch(v & np.uint64(0xFFFFF)), ms.dyn_bp(512))
+    assert narrow.max_width == 20
+    # a hint that understates the widths of two adjacent wide blocks would overrun a
+    # narrow staging slot: detected (MS_E_CORRUPT), never decoded out of bounds
+    v2 = v.copy()
+    v2[512 * 4 + 7] = (1 << 40) + 1
+    v2[512 * 5 + 9] = (1 << 40) + 2
+    c2 = ms.compress(to_torch(v2), ms.dyn_bp(512))
+    c2._c.fmt.max_width = 20
+    with pytest.raises(ms.MsError) as e:
+        ms.select(c2, ms.LT, 1 << 16, out_fmt=ms.delta_bp(512))
+    assert e.value.code == 5  # MS_E_CORRUPT
+    # a hint that is wrong but harmless still gives the exact result
+    c._c.fmt.max_width = 20
+    gs = ms.select(c, ms.LT, 1 << 16, out_fmt=ms.delta_bp(512))
+    assert_same_image(gs, O.select(O.encode(v, O.DYN_BP, 0, 512), O.LT, 1 << 16, out_fmt=O.DELTA_BP,
+                                   out_block=512), "select with understated hint")
