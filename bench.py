@@ -296,7 +296,7 @@ def run_ours(args):
     alg = {"select_fast": x_bytes,                                 # compressed X read
            "pos_encode": bytes_pos,                                # positions image written
            "project_warp": gather_bytes + bytes_yp,                # positions + touched Y + Y' written
-           "sum": bytes_yp}                                        # Y' read
+           "sum_fast": bytes_yp}                                   # Y' read
     kernels = {}
     for k, (launches, tot_ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         avg = tot_ms / max(1, launches)

@@ -266,6 +266,7 @@ ms_status maybe_shrink(const Ctx& ctx, ms_column* out) {
   ms_column t;
   MS_TRY(alloc_column(ctx, &t, out->fmt, out->n, out->payload_words, out->n_runs));
   t.payload_words = out->payload_words;
+  t.fmt.max_width = out->fmt.max_width;
   MS_TRY_CUDA(cudaMemcpyAsync(t.payload, out->payload, 8 * out->payload_words, cudaMemcpyDeviceToDevice, ctx.s));
   MS_TRY_CUDA(cudaMemcpyAsync(t.cw, out->cw, 4 * (out->n_blocks + 1), cudaMemcpyDeviceToDevice, ctx.s));
   if (out->ref && out->n_blocks)

@@ -63,12 +63,16 @@ __device__ __forceinline__ uint64_t unpack_at(const uint64_t* __restrict__ p, ui
   return v & low_mask(w);
 }
 
-// volatile 64-bit status words (single-copy atomic when aligned)
+// 64-bit look-back status words: GPU-scope relaxed accesses (single-copy
+// atomic; the flag and the value travel in the same word, so no ordering with
+// other data is needed). `volatile` would compile to system-scope loads.
 __device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
-  return *reinterpret_cast<const volatile uint64_t*>(p);
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
-  *reinterpret_cast<volatile uint64_t*>(p) = v;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // ------------------------------------------------------------ scans

@@ -250,7 +250,7 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
       const uint64_t used = (ns_fast + spw - 1) / spw;
       const int grid = (int)((used + warps_per_cta - 1) / warps_per_cta);
       ProfScope prof_("select_fast", s);
-      k<<<grid, warps_per_cta * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw, err);
+      k<<<grid, warps_per_cta * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw, err, nullptr);
     };
     // variants (stages, warps/CTA, min CTAs/SM); default measured on B200, env override for experiments
     const int v = env_int("MS_SELECT_VARIANT", 0);
@@ -584,9 +584,62 @@ __global__ void __launch_bounds__(kThreads) sum_kernel(ColView c, unsigned long 
   }
 }
 
+// rows [r0, n) of a column, one value at a time (the tail the fast scan leaves)
+__global__ void sum_rows_kernel(ColView c, uint64_t r0, unsigned long long* out) {
+  uint64_t acc = 0;
+  for (uint64_t r = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < c.n; r += (uint64_t)gridDim.x * blockDim.x)
+    acc += read_row(c, r);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
 cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err, cudaStream_t s) {
-  ProfScope prof_("sum", s);
-  sum_kernel<<<persistent_grid(sum_kernel, kThreads, ~0ull), kThreads, 0, s>>>(c, out);
+  // fast path: the select scan machinery with a sum core, over full 512-row segments
+  int kind = -1;
+  uint64_t ns_fast = 0;
+  if (c.format == MS_UNCOMPR) { kind = FAST_UNCOMPR; ns_fast = c.n / kSegRows; }
+  if (c.format == MS_STATIC_BP) { kind = FAST_STATIC; ns_fast = c.n / kSegRows; }
+  if ((c.format == MS_DYN_BP || c.format == MS_FOR_BP) && c.B >= (uint32_t)kSegRows) {
+    kind = FAST_BLOCK;
+    ns_fast = (c.nb << c.log2B) / kSegRows;
+  }
+  if (kind < 0 || !ns_fast) {
+    ProfScope prof_("sum", s);
+    sum_kernel<<<persistent_grid(sum_kernel, kThreads, ~0ull), kThreads, 0, s>>>(c, out);
+    return cudaGetLastError();
+  }
+  const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
+  FastPred fp{};
+  auto pick = [&](auto k, int bufu32) {
+    const size_t smem = (size_t)4 * 2 * bufu32 * 4;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 4 * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t warps = (uint64_t)per_sm * num_sms() * 4;
+    uint64_t spw = (ns_fast + warps - 1) / warps;
+    spw += spw & 1;
+    const uint64_t used = (ns_fast + spw - 1) / spw;
+    const int grid = (int)((used + 3) / 4);
+    ProfScope prof_("sum_fast", s);
+    k<<<grid, 4 * 32, smem, s>>>(c, fp, nullptr, nullptr, ns_fast, spw, err, out);
+  };
+#define MS_PICK_SUM(K)                                                                               \
+  do {                                                                                               \
+    if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow, CORE_SUM>, kPairBufNarrow);      \
+    else pick(select_fast_kernel<K, 2, 4, 3, kPairBufWide, CORE_SUM>, kPairBufWide);                 \
+  } while (0)
+  if (kind == FAST_UNCOMPR) MS_PICK_SUM(FAST_UNCOMPR);
+  else if (kind == FAST_STATIC) MS_PICK_SUM(FAST_STATIC);
+  else MS_PICK_SUM(FAST_BLOCK);
+#undef MS_PICK_SUM
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const uint64_t r0 = ns_fast * kSegRows;
+  if (r0 < c.n) {
+    ProfScope prof_("sum_tail", s);
+    sum_rows_kernel<<<8, 256, 0, s>>>(c, r0, out);
+  }
   return cudaGetLastError();
 }
 
@@ -686,7 +739,7 @@ static cudaError_t run_warp_encode(const Src& src, const PosEnc& e, uint64_t* st
   if (!n_items) return cudaSuccess;
   auto k = warp_encode_kernel<Src>;
   const int warps = e.G >= 2048 ? 2 : 4;
-  const size_t smem = (size_t)warps * e.G * 8;
+  const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);

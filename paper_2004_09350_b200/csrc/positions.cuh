@@ -23,6 +23,12 @@ __device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
   return __ffs(x) - 1;
 }
 
+// Shared-memory tile index with one pad slot every 16 entries: keeps both the
+// lane-consecutive (16 entries per lane) and the lane-strided access patterns
+// of the 8-byte tile free of bank conflicts.
+__device__ __forceinline__ uint32_t pidx(uint32_t i) { return i + (i >> 4); }
+__host__ __device__ constexpr uint32_t tile_slots(uint32_t G) { return G + G / 16 + 2; }
+
 // ------------------------------------------------------------------ sources
 // select: expand the item's positions from the mask, starting at gstart[item]
 struct MaskSource {
@@ -60,7 +66,7 @@ struct MaskSource {
         while (word && k < cnt) {
           const int b = __ffs(word) - 1;
           word &= word - 1;
-          P[k++] = base + b;
+          P[pidx(k++)] = base + b;
         }
         got += __shfl_sync(kFull, incl, 31);
       }
@@ -96,23 +102,24 @@ struct ProjectSource {
       uint64_t acc = 0;
       for (uint32_t q = 0; q < per; ++q) {
         acc += unpack_at(pos.payload, bit0 + (uint64_t)(lane * per + q) * w, w);
-        P[lane * per + q] = acc;
+        P[pidx(lane * per + q)] = acc;
       }
       uint64_t incl = warp_incl_scan(acc);
       const uint64_t base = __ldg(pos.ref + b) + incl - acc;
       __syncwarp();
-      for (uint32_t q = 0; q < per; ++q) P[lane * per + q] += base;
+      for (uint32_t q = 0; q < per; ++q) P[pidx(lane * per + q)] += base;
     } else {
-      for (uint32_t i = lane; i < cnt; i += 32) P[i] = read_row(pos, r0 + i);
+      for (uint32_t i = lane; i < cnt; i += 32) P[pidx(i)] = read_row(pos, r0 + i);
     }
     __syncwarp();
     // ---- gather
     if (data.format == MS_DYN_BP || data.format == MS_FOR_BP) {
       const uint64_t main_rows = data.nb << data.log2B;
-      const uint64_t plo = P[0] - row_offset, phi = P[cnt - 1] - row_offset;  // sorted positions
+      const uint64_t p_first = P[pidx(0)], p_last = P[pidx(cnt - 1)];
+      const uint64_t plo = p_first - row_offset, phi = p_last - row_offset;  // sorted positions
       const uint64_t b_lo = plo >> data.log2B;
-      const bool window = P[0] >= row_offset && phi < main_rows && ((phi >> data.log2B) - b_lo) < 32 &&
-                          P[cnt - 1] >= P[0];
+      const bool window = p_first >= row_offset && phi < main_rows && ((phi >> data.log2B) - b_lo) < 32 &&
+                          p_last >= p_first;
       uint32_t h_cw = 0;
       uint64_t h_ref = 0;
       if (window) {
@@ -143,7 +150,7 @@ struct ProjectSource {
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
-          const uint64_t p = i < cnt ? P[i] : row_offset;
+          const uint64_t p = i < cnt ? P[pidx(i)] : row_offset;
           const bool ok = p >= row_offset && p - row_offset < data.n;
           if (i < cnt && !ok) atomicOr(err, err_bit(MS_E_RANGE));
           const uint64_t r = ok ? p - row_offset : 0;
@@ -172,16 +179,16 @@ struct ProjectSource {
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
-          if (i < cnt) P[i] = v[q];
+          if (i < cnt) P[pidx(i)] = v[q];
         }
       }
     } else {
       for (uint32_t i = lane; i < cnt; i += 32) {
-        const uint64_t p = P[i];
+        const uint64_t p = P[pidx(i)];
         uint64_t v = 0;
         if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
         else v = read_row(data, p - row_offset);
-        P[i] = v;
+        P[pidx(i)] = v;
       }
     }
     __syncwarp();
@@ -203,10 +210,10 @@ __device__ __forceinline__ void encode_finish(const PosEnc& e, uint32_t item, ui
   const uint64_t r0 = (uint64_t)item * e.G;
   if (!is_block) {
     if (e.format == MS_UNCOMPR) {
-      for (uint32_t i = lane; i < cnt; i += 32) e.payload[r0 + i] = P[i];
+      for (uint32_t i = lane; i < cnt; i += 32) e.payload[r0 + i] = P[pidx(i)];
     } else if (e.format == MS_RLE) {
       for (uint32_t i = lane; i < cnt; i += 32) {
-        e.payload[2 * (r0 + i)] = P[i];
+        e.payload[2 * (r0 + i)] = P[pidx(i)];
         e.payload[2 * (r0 + i) + 1] = 1;
       }
     } else {  // STATIC_BP: item = ranks [512k, 512k+cnt) at bit 512k*w (word aligned)
@@ -219,11 +226,11 @@ __device__ __forceinline__ void encode_finish(const PosEnc& e, uint32_t item, ui
         const uint32_t bit0 = m * 64;
         uint32_t j = div_small(bit0, ws, magic);
         const uint32_t sft = bit0 - j * ws;
-        uint64_t acc = (P[j] & mask) >> sft;
+        uint64_t acc = (P[pidx(j)] & mask) >> sft;
         for (++j; j < cnt; ++j) {
           const uint32_t jb = j * ws;
           if (jb >= bit0 + 64) break;
-          acc |= (P[j] & mask) << (jb - bit0);
+          acc |= (P[pidx(j)] & mask) << (jb - bit0);
         }
         e.payload[wbase + m] = acc;
       }
@@ -231,14 +238,14 @@ __device__ __forceinline__ void encode_finish(const PosEnc& e, uint32_t item, ui
     return;
   }
   if (cnt < e.G) {  // final partial block -> uncompressed remainder
-    for (uint32_t i = lane; i < cnt; i += 32) e.rem[i] = P[i];
+    for (uint32_t i = lane; i < cnt; i += 32) e.rem[i] = P[pidx(i)];
     return;
   }
   const uint64_t E = lookback_resolve(status, item, w);
   if (lane == 0) {
     if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
     e.cw[item + 1] = (uint32_t)(E + w);
-    if (e.format == MS_DELTA_BP) e.ref[item] = P[0];
+    if (e.format == MS_DELTA_BP) e.ref[item] = P[pidx(0)];
     if (e.format == MS_FOR_BP) e.ref[item] = rmin;
   }
   if (!w) return;
@@ -250,9 +257,9 @@ __device__ __forceinline__ void encode_finish(const PosEnc& e, uint32_t item, ui
     uint32_t j = div_small(bit0, w, magic);
     const uint32_t sft = bit0 - j * w;
     auto code = [&](uint32_t i) -> uint64_t {
-      if (e.format == MS_DELTA_BP) return i ? P[i] - P[i - 1] : 0ull;
-      if (e.format == MS_FOR_BP) return P[i] - rmin;
-      return P[i];
+      if (e.format == MS_DELTA_BP) return i ? P[pidx(i)] - P[pidx(i - 1)] : 0ull;
+      if (e.format == MS_FOR_BP) return P[pidx(i)] - rmin;
+      return P[pidx(i)];
     };
     uint64_t acc = code(j) >> sft;
     for (++j; j < cnt; ++j) {
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__(128) warp_encode_kernel(Src src, PosEnc e, uin
                                                           uint32_t* ticket, uint32_t* err) {
   extern __shared__ __align__(16) uint64_t enc_sm[];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint64_t* P = enc_sm + (uint64_t)wid * e.G;
+  uint64_t* P = enc_sm + (uint64_t)wid * tile_slots(e.G);
   const bool is_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
   while (true) {
     uint32_t item = 0;
@@ -285,15 +292,16 @@ __global__ void __launch_bounds__(128) warp_encode_kernel(Src src, PosEnc e, uin
       uint64_t mx = 0;
       if (e.format == MS_DELTA_BP) {
         for (uint32_t i = lane; i < cnt; i += 32) {
-          const uint64_t d = i ? P[i] - P[i - 1] : 0ull;
+          const uint64_t d = i ? P[pidx(i)] - P[pidx(i - 1)] : 0ull;
           mx = d > mx ? d : mx;
         }
         mx = warp_max(mx);
       } else {  // FOR: ebw(max - min); DYN: ebw(max) (values need not be sorted: project)
         uint64_t lo = ~0ull, hi = 0;
         for (uint32_t i = lane; i < cnt; i += 32) {
-          lo = P[i] < lo ? P[i] : lo;
-          hi = P[i] > hi ? P[i] : hi;
+          const uint64_t x = P[pidx(i)];
+          lo = x < lo ? x : lo;
+          hi = x > hi ? x : hi;
         }
         hi = warp_max(hi);
         if (e.format == MS_FOR_BP) {

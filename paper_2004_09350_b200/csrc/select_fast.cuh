@@ -229,6 +229,60 @@ __device__ __forceinline__ uint32_t lane_dispatch(uint32_t w, const uint32_t* p,
   }
 }
 
+// ---- sum core: the same lane-consecutive unpack, accumulating the codes
+template <int W>
+__device__ __forceinline__ uint64_t lane_sum(const uint32_t* __restrict__ p) {
+  if constexpr (W == 0) {
+    return 0;
+  } else if constexpr (W <= 32) {
+    uint32_t r[W + 1];
+    load_words<W>(p, r);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc += code_at<W>(r, i);
+    return acc;
+  } else {
+    uint64_t acc = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int B0 = h * 16 * W, Q0 = B0 >> 5;
+      constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int bit = (B0 & 31) + i * W, q = Q0 + (bit >> 5), sh = bit & 31;
+        const uint32_t w0 = p[q], w1 = q + 1 < W ? p[q + 1] : 0u, w2 = q + 2 < W ? p[q + 2] : 0u;
+        const uint64_t code = (((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh)) & mask;
+        acc += code;
+      }
+    }
+    return acc;
+  }
+}
+
+__device__ __forceinline__ uint64_t lane_sum_dispatch(uint32_t w, const uint32_t* p) {
+  switch (w) {
+#define MS_SUM_CASE(W) \
+  case W:              \
+    return lane_sum<W>(p);
+    MS_SUM_CASE(0) MS_SUM_CASE(1) MS_SUM_CASE(2) MS_SUM_CASE(3) MS_SUM_CASE(4) MS_SUM_CASE(5) MS_SUM_CASE(6)
+    MS_SUM_CASE(7) MS_SUM_CASE(8) MS_SUM_CASE(9) MS_SUM_CASE(10) MS_SUM_CASE(11) MS_SUM_CASE(12)
+    MS_SUM_CASE(13) MS_SUM_CASE(14) MS_SUM_CASE(15) MS_SUM_CASE(16) MS_SUM_CASE(17) MS_SUM_CASE(18)
+    MS_SUM_CASE(19) MS_SUM_CASE(20) MS_SUM_CASE(21) MS_SUM_CASE(22) MS_SUM_CASE(23) MS_SUM_CASE(24)
+    MS_SUM_CASE(25) MS_SUM_CASE(26) MS_SUM_CASE(27) MS_SUM_CASE(28) MS_SUM_CASE(29) MS_SUM_CASE(30)
+    MS_SUM_CASE(31) MS_SUM_CASE(32) MS_SUM_CASE(33) MS_SUM_CASE(34) MS_SUM_CASE(35) MS_SUM_CASE(36)
+    MS_SUM_CASE(37) MS_SUM_CASE(38) MS_SUM_CASE(39) MS_SUM_CASE(40) MS_SUM_CASE(41) MS_SUM_CASE(42)
+    MS_SUM_CASE(43) MS_SUM_CASE(44) MS_SUM_CASE(45) MS_SUM_CASE(46) MS_SUM_CASE(47) MS_SUM_CASE(48)
+    MS_SUM_CASE(49) MS_SUM_CASE(50) MS_SUM_CASE(51) MS_SUM_CASE(52) MS_SUM_CASE(53) MS_SUM_CASE(54)
+    MS_SUM_CASE(55) MS_SUM_CASE(56) MS_SUM_CASE(57) MS_SUM_CASE(58) MS_SUM_CASE(59) MS_SUM_CASE(60)
+    MS_SUM_CASE(61) MS_SUM_CASE(62) MS_SUM_CASE(63) MS_SUM_CASE(64)
+#undef MS_SUM_CASE
+    default:
+      return 0;
+  }
+}
+
+enum : int { CORE_SELECT = 0, CORE_SUM = 1 };
+
 // Per-warp contiguous range of full 512-row segments, taken two at a time
 // (half-warp h handles segment 2p+h). Lane 0 streams the pair's packed payload
 // (64*(wA+wB) bytes, contiguous, 64-byte aligned) into a per-warp ring of
@@ -236,12 +290,14 @@ __device__ __forceinline__ uint32_t lane_dispatch(uint32_t w, const uint32_t* p,
 // widths / references travel with the slot.
 constexpr int kPairBufWide = 2048 + 16;   // two segments at up to 64 bits + padding
 constexpr int kPairBufNarrow = 1024 + 16; // two segments at up to 32 bits + padding
-template <int KIND, int kStages = 2, int kFastWarps = 4, int kMinBlocks = 3, int kPairBufU32 = kPairBufWide>
+template <int KIND, int kStages = 2, int kFastWarps = 4, int kMinBlocks = 3, int kPairBufU32 = kPairBufWide,
+          int CORE = CORE_SELECT>
 __global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kernel(ColView c, FastPred pred,
                                                                                  uint32_t* __restrict__ bits,
                                                                                  uint32_t* __restrict__ seg_info,
                                                                                  uint64_t NS, uint64_t spw,
-                                                                                 uint32_t* err) {
+                                                                                 uint32_t* err,
+                                                                                 unsigned long long* sum_out) {
   extern __shared__ __align__(128) uint32_t fsm[];
   __shared__ __align__(8) uint64_t bars[kFastWarps][kStages];
   __shared__ uint64_t sref[kFastWarps][kStages][2];
@@ -299,6 +355,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kerne
   for (int k = 0; k < kStages - 1; ++k) issue(s_begin + 2 * k, k);
   int stage = 0;
   uint32_t phase = 0;
+  uint64_t sum_acc = 0;
   for (uint64_t s = s_begin; s < s_end; s += 2) {
     issue(s + 2 * (kStages - 1), (stage + kStages - 1) % kStages);
     const uint64_t my_seg = s + half;
@@ -313,12 +370,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kerne
           const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(v + i));
           x[i] = t.x; x[i + 1] = t.y;
         }
+        if constexpr (CORE == CORE_SUM) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          bool keep;
-          if (pred.is_bitmap) keep = x[i] < pred.bits && ((__ldg(pred.bitmap + (x[i] >> 6)) >> (x[i] & 63)) & 1ull);
-          else keep = ((x[i] - pred.lo) <= pred.span) != (pred.neg != 0);
-          m |= (keep ? 1u : 0u) << i;
+          for (int i = 0; i < 32; ++i) sum_acc += x[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            bool keep;
+            if (pred.is_bitmap) keep = x[i] < pred.bits && ((__ldg(pred.bitmap + (x[i] >> 6)) >> (x[i] & 63)) & 1ull);
+            else keep = ((x[i] - pred.lo) <= pred.span) != (pred.neg != 0);
+            m |= (keep ? 1u : 0u) << i;
+          }
         }
       }
     } else {
@@ -327,22 +389,34 @@ __global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kerne
       const uint32_t w = sw[wid][stage][half];
       const uint64_t ref = sref[wid][stage][half];
       const uint32_t* p = buf + stage * kPairBufU32 + (half ? 16 * wa : 0) + hl * w;
-      if (valid) m = lane_dispatch(w, p, pred, ref);
+      if (valid) {
+        if constexpr (CORE == CORE_SUM) {
+          sum_acc += lane_sum_dispatch(w, p) + (hl == 0 ? (uint64_t)kSegRows * ref : 0ull);
+        } else {
+          m = lane_dispatch(w, p, pred, ref);
+        }
+      }
     }
     __syncwarp();
-    if (valid) bits[my_seg * kSegWords + hl] = m;
-    uint32_t cnt = __popc(m);
-    uint32_t last = m ? hl * 32 + 32 - __clz(m) : 0u;
+    if constexpr (CORE == CORE_SELECT) {
+      if (valid) bits[my_seg * kSegWords + hl] = m;
+      uint32_t cnt = __popc(m);
+      uint32_t last = m ? hl * 32 + 32 - __clz(m) : 0u;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-      cnt += __shfl_xor_sync(kFull, cnt, o);
-      last = max(last, __shfl_xor_sync(kFull, last, o));
+      for (int o = 8; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(kFull, cnt, o);
+        last = max(last, __shfl_xor_sync(kFull, last, o));
+      }
+      if (valid && hl == 0) seg_info[my_seg] = cnt | (last << 16);
     }
-    if (valid && hl == 0) seg_info[my_seg] = cnt | (last << 16);
     if (++stage == kStages) {
       stage = 0;
       phase ^= 1u;
     }
+  }
+  if constexpr (CORE == CORE_SUM) {
+    sum_acc = warp_sum(sum_acc);
+    if (lane == 0 && sum_acc) atomicAdd(sum_out, (unsigned long long)sum_acc);
   }
 }
 
