@@ -298,9 +298,9 @@ def run_ours(args):
            "project_warp": gather_bytes + bytes_yp,                # positions + touched Y + Y' written
            "sum_fast": bytes_yp}                                   # Y' read
     kernels = {}
-    for k, (launches, tot_ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
-        avg = tot_ms / max(1, launches)
-        ent = {"launches": launches, "avg_ms": avg, "share": tot_ms / ms_total}
+    for k, (k_launches, tot_ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        avg = tot_ms / max(1, k_launches)
+        ent = {"launches": k_launches, "avg_ms": avg, "share": tot_ms / ms_total}
         if k in alg:
             ent["alg_bytes"] = alg[k]
             ent["achieved_gbs"] = alg[k] / (avg * 1e-3) / 1e9
