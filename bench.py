@@ -293,9 +293,13 @@ def run_ours(args):
     x_bytes, y_bytes = X.footprint(), Y.footprint()
     gather_bytes = touched_gather_bytes(X, Y, start, pos_fmt)  # positions + touched Y sectors/headers
     # algorithmic bytes per launch: what the method itself must move
-    alg = {"select_fast": x_bytes,                                 # compressed X read
-           "pos_encode": bytes_pos,                                # positions image written
-           "project_warp": gather_bytes + bytes_yp,                # positions + touched Y + Y' written
+    mask_bytes = 4 * 16 * ((m + 511) // 512)                       # select's 1-bit-per-row match mask
+    alg = {"select_fast": x_bytes + mask_bytes,                    # compressed X read, mask written
+           "pos_width": mask_bytes,                                # mask read
+           "pos_pack": mask_bytes + bytes_pos,                     # mask read, positions image written
+           "pos_encode": mask_bytes + bytes_pos,
+           "project_fast": gather_bytes + bytes_yp,                # positions + touched Y + Y' written
+           "project_warp": gather_bytes + bytes_yp,
            "sum_fast": bytes_yp}                                   # Y' read
     kernels = {}
     for k, (k_launches, tot_ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):

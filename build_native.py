@@ -56,27 +56,48 @@ def build_oracle(force=False):
               "-o", so, *srcs])
 
 
+def _local_deps(path, dirs, seen=None):
+    """The file plus every quoted #include it pulls in (recursively) from dirs."""
+    import re
+    seen = set() if seen is None else seen
+    if path in seen:
+        return seen
+    seen.add(path)
+    for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', open(path).read(), re.M):
+        for d in dirs:
+            q = os.path.join(d, inc)
+            if os.path.exists(q):
+                _local_deps(q, dirs, seen)
+                break
+    return seen
+
+
 def build_libms(force=False):
+    from concurrent.futures import ThreadPoolExecutor
     pkg = os.path.join(ROOT, "paper_2004_09350_b200")
     csrc = os.path.join(pkg, "csrc")
+    inc = os.path.join(ROOT, "include")
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
-    hdrs = sorted(glob.glob(os.path.join(csrc, "*.cuh"))) + sorted(
-        glob.glob(os.path.join(ROOT, "include", "*.h")))
     so = os.path.join(pkg, "libms.so")
-    if not srcs or not (force or _stale(so, srcs + hdrs)):
-        return
     objdir = os.path.join(ROOT, "build", "libms")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
     flags = [*ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
-             "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"), "-I", csrc,
+             "-fvisibility=hidden", "-I", inc, "-I", csrc,
              "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+    objs, jobs = [], []
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        if force or _stale(o, [s] + hdrs):
-            _run([NVCC, *flags, "-c", "-o", o, s])
+        if force or _stale(o, sorted(_local_deps(s, [csrc, inc]))):
+            jobs.append([NVCC, *flags, "-c", "-o", o, s])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart"])
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+            list(ex.map(_run, jobs))
+    stale_objs = [o for o in glob.glob(os.path.join(objdir, "*.o")) if o not in objs]
+    for o in stale_objs:  # objects of sources that no longer exist
+        os.unlink(o)
+    if force or jobs or _stale(so, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart"])
 
 
 def build_all(force=False):

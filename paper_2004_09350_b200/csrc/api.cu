@@ -599,6 +599,11 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t o_tk1 = sc.add(8, true);
   const uint64_t o_st2 = sc.add(8 * (items_max + 1), true);
   const uint64_t o_tk2 = sc.add(8, true);
+  const bool pos_delta = out_fmt.format == MS_DELTA_BP && G <= 512;  // posdelta.cuh
+  const uint64_t o_wk = pos_delta ? sc.add(4 * (items_max + 1), false) : 0;
+  const uint64_t o_cwx = pos_delta ? sc.add(8 * (items_max + 2), false) : 0;
+  const uint64_t o_st3 = pos_delta ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
+  const uint64_t o_tk3 = pos_delta ? sc.add(8, true) : 0;
   RlePrep rp;
   plan_rle(sc, in, rp);
   if (!sc.commit()) return MS_E_NOMEM;
@@ -662,8 +667,13 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
     pe.cw = out->cw;
     pe.ref = out->ref;
     pe.rem = out->rem;
-    cudaError_t e = launch_positions(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
-                                     sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
+    cudaError_t e =
+        pos_delta && f.format == MS_DELTA_BP
+            ? launch_positions_delta(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
+                                     sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
+                                     sc.at<uint32_t>(o_tk3), err, ctx.s)
+            : launch_positions(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
+                               sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
     if (e != cudaSuccess) {
       release(ctx, out);
       return cuda_status(e);

@@ -127,6 +127,47 @@ __device__ __forceinline__ uint64_t cta_excl_scan(uint64_t v, uint64_t* sm, uint
 // CTAs (no deadlock).
 constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
+// Exclusive prefix of item t (t >= 1) from the status words of its
+// predecessors; call with ALL 32 lanes of ONE warp. Each round reads a window of
+// 128 predecessors (lane j: items base-4j .. base-4j-3, four independent loads
+// in flight), spins only on the ones not yet published, and stops at the first
+// inclusive prefix (flag P) in descending item order. The window width sets how
+// fast the P frontier can advance (128 items per L2 round trip).
+__device__ __forceinline__ uint64_t lookback_walk(const uint64_t* status, uint64_t t) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t base = (int64_t)t - 1;
+  while (true) {
+    uint64_t s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t idx = base - 4 * lane - i;
+      s[i] = idx >= 0 ? ld_volatile(&status[idx]) : kFlagP;  // before item 0: prefix 0
+    }
+    int spins = 0;
+    while (((s[0] >> 62) == 0) | ((s[1] >> 62) == 0) | ((s[2] >> 62) == 0) | ((s[3] >> 62) == 0)) {
+      if (++spins > 4) __nanosleep(32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((s[i] >> 62) == 0) s[i] = ld_volatile(&status[base - 4 * lane - i]);
+    }
+    int first_i = 4;
+#pragma unroll
+    for (int i = 3; i >= 0; --i)
+      if ((s[i] >> 62) == 2) first_i = i;
+    const unsigned pmask = __ballot_sync(kFull, first_i < 4);
+    const int first_lane = pmask ? __ffs(pmask) - 1 : 32;
+    uint64_t v = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane < first_lane || (lane == first_lane && i <= first_i)) v += s[i] & kValMask;
+    excl += warp_sum(v);
+    if (pmask) break;
+    base -= 128;
+  }
+  return excl & kValMask;
+}
+
 // Call with ALL 32 lanes of ONE warp. Returns the exclusive prefix of item t.
 __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, uint64_t t, uint64_t agg) {
   const int lane = threadIdx.x & 31;
@@ -135,54 +176,20 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, uint64_t t, 
     return 0;
   }
   if (lane == 0) st_volatile(&status[t], kFlagA | agg);
-  uint64_t excl = 0;
-  int64_t base = (int64_t)t - 1;
-  while (true) {
-    const int64_t idx = base - lane;
-    uint64_t s = kFlagP;  // before item 0: prefix 0
-    if (idx >= 0) {
-      int spins = 0;
-      while (((s = ld_volatile(&status[idx])) >> 62) == 0) {
-        if (++spins > 8) __nanosleep(64);
-      }
-    }
-    const unsigned pmask = __ballot_sync(kFull, (s >> 62) == 2);
-    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
-    uint64_t v = (lane <= first_p) ? (s & kValMask) : 0;
-    excl += warp_sum(v);
-    if (pmask) break;
-    base -= 32;
-  }
+  const uint64_t excl = lookback_walk(status, t);
   if (lane == 0) st_volatile(&status[t], kFlagP | ((excl + agg) & kValMask));
   return excl;
 }
 
-// Split look-back for software-pipelined items: publish the aggregate early,
-// resolve the exclusive prefix later (by then the predecessors are done).
+// Split look-back: publish the aggregate early, resolve the exclusive prefix
+// later (by then the predecessors have had time to publish theirs).
 __device__ __forceinline__ void lookback_publish(uint64_t* status, uint64_t t, uint64_t agg) {
   if ((threadIdx.x & 31) == 0) st_volatile(&status[t], (t == 0 ? kFlagP : kFlagA) | agg);
 }
 __device__ __forceinline__ uint64_t lookback_resolve(uint64_t* status, uint64_t t, uint64_t agg) {
   const int lane = threadIdx.x & 31;
   if (t == 0) return 0;
-  uint64_t excl = 0;
-  int64_t base = (int64_t)t - 1;
-  while (true) {
-    const int64_t idx = base - lane;
-    uint64_t s = kFlagP;
-    if (idx >= 0) {
-      int spins = 0;
-      while (((s = ld_volatile(&status[idx])) >> 62) == 0) {
-        if (++spins > 8) __nanosleep(64);
-      }
-    }
-    const unsigned pmask = __ballot_sync(kFull, (s >> 62) == 2);
-    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
-    uint64_t v = (lane <= first_p) ? (s & kValMask) : 0;
-    excl += warp_sum(v);
-    if (pmask) break;
-    base -= 32;
-  }
+  const uint64_t excl = lookback_walk(status, t);
   if (lane == 0) st_volatile(&status[t], kFlagP | ((excl + agg) & kValMask));
   return excl;
 }
@@ -195,6 +202,12 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, uint32_t m
   if (q * w > x) --q;
   if ((q + 1) * w <= x) ++q;
   return q;
+}
+
+// select-in-word: position of the (k+1)-th set bit of x (k < popc(x))
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
+  for (uint32_t i = 0; i < k; ++i) x &= x - 1;
+  return __ffs(x) - 1;
 }
 
 // ---------------------------------------------------------- random access

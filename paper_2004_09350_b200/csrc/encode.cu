@@ -1,0 +1,143 @@
+// encode.cu — output-side buffer layers: select positions (posdelta.cuh for
+// DELTA_BP, positions.cuh otherwise) and project's gather + re-encode.
+#include "common.cuh"
+#include "grid.cuh"
+#include "positions.cuh"
+#include "posdelta.cuh"
+#include "project.cuh"
+#include "launch.h"
+
+namespace ms {
+
+// ------------------------------------------------- select output encoder
+template <class Src>
+static cudaError_t run_warp_encode(const Src& src, const PosEnc& e, uint64_t* status, uint32_t* ticket,
+                                   uint32_t* err, const char* name, cudaStream_t s) {
+  const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
+  if (!n_items) return cudaSuccess;
+  if (e.G <= 512 && !env_int("MS_ENCODE_TICKET", 0)) {  // deferred look-back, two tiles per warp
+    auto launch = [&](auto k) {
+      const int warps = 4;
+      const size_t smem = (size_t)warps * 2 * tile_slots(e.G) * 8;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+  if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
+      if (per_sm < 1) per_sm = 1;
+      uint64_t grid = (uint64_t)per_sm * num_sms();
+      const uint64_t need = (n_items + warps - 1) / warps;
+      if (need < grid) grid = need;
+      ProfScope prof_(name, s);
+      k<<<(int)grid, warps * 32, smem, s>>>(src, e, n_items, status, ticket, err);
+      return cudaGetLastError();
+    };
+    if (e.G == 512) return launch(warp_encode_deferred_kernel<Src, 16>);
+    if (e.G == 256) return launch(warp_encode_deferred_kernel<Src, 8>);
+    return launch(warp_encode_deferred_kernel<Src, 4>);
+  }
+  auto k = warp_encode_kernel<Src>;
+  const int warps = e.G >= 2048 ? 2 : 4;
+  const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+  if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)per_sm * num_sms();
+  const uint64_t need = (n_items + warps - 1) / warps;
+  if (need < grid) grid = need;
+  ProfScope prof_(name, s);
+  k<<<(int)grid, warps * 32, smem, s>>>(src, e, n_items, status, ticket, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                             uint64_t row_offset, uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {
+  return run_warp_encode(MaskSource{bits, NS, gstart, row_offset}, e, status, ticket, err, "pos_encode", s);
+}
+
+
+cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                                   uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
+                                   uint32_t* scan_ticket, uint32_t* err, cudaStream_t s) {
+  const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
+  const uint64_t n_full = e.n_out / e.G;
+  if (!n_items) return cudaSuccess;
+  const uint64_t n_words = NS * kSegWords;
+  auto grid_for = [&](auto k, size_t smem, uint64_t items) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPdWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t g = (uint64_t)per_sm * num_sms();
+    const uint64_t need = (items + kPdWarps - 1) / kPdWarps;
+    return (int)(need < g ? (need ? need : 1) : g);
+  };
+  if (n_full) {
+    const size_t smem = (size_t)kPdWarps * kPdStageU32 * 4;
+    const int grid = grid_for(pos_width_kernel, smem, n_full);
+    {
+      ProfScope prof_("pos_width", s);
+      pos_width_kernel<<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e.G, n_full, n_items,
+                                                          wk, err);
+    }
+    cudaError_t r = cudaGetLastError();
+    if (r != cudaSuccess) return r;
+    r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
+    if (r != cudaSuccess) return r;
+  }
+  const size_t smem = (size_t)kPdWarps * kPdWarpU32 * 4;
+  const int grid = grid_for(pos_pack_kernel, smem, n_items);
+  ProfScope prof_("pos_pack", s);
+  pos_pack_kernel<<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items, cwx, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
+                                uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {
+  // register-resident path: DELTA_BP{G} positions, header-addressed data, block output of size G or UNCOMPR
+  const bool out_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  const uint32_t pf = (uint32_t)env_int("MS_GATHER_PREFETCH", 1);
+  if (pos.format == MS_DELTA_BP && pos.B == e.G && e.G >= 128 && e.G <= 512 &&
+      (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && env_int("MS_PROJECT_FAST", 0)) {
+    if (e.G == 512) return run_warp_encode(ProjectFastSource<16>{pos, data, row_offset, pf}, e, status, ticket, err,
+                                           "project_fast", s);
+    if (e.G == 256) return run_warp_encode(ProjectFastSource<8>{pos, data, row_offset, pf}, e, status, ticket, err,
+                                           "project_fast", s);
+    return run_warp_encode(ProjectFastSource<4>{pos, data, row_offset, pf}, e, status, ticket, err, "project_fast", s);
+  }
+  if (pos.format == MS_DELTA_BP && pos.B == e.G && e.G >= 128 && e.G <= 512 &&
+      (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && (out_block || e.format == MS_UNCOMPR) &&
+      env_int("MS_PROJECT_REGS", 0)) {
+    const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
+    if (!n_items) return cudaSuccess;
+    auto launch = [&](auto k) {
+      const int warps = 4;
+      const size_t smem = (size_t)warps * 2 * (2 * e.G) * 4;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+  if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
+      if (per_sm < 1) per_sm = 1;
+      uint64_t grid = (uint64_t)per_sm * num_sms();
+      const uint64_t need = (n_items + warps - 1) / warps;
+      if (need < grid) grid = need;
+      ProfScope prof_("project_regs", s);
+      k<<<(int)grid, warps * 32, smem, s>>>(pos, data, row_offset, e, n_items, status, ticket, err,
+                                            (uint32_t)env_int("MS_GATHER_PREFETCH", 1));
+      return cudaGetLastError();
+    };
+    if (e.G == 512) return launch(project_fast_kernel<16>);
+    if (e.G == 256) return launch(project_fast_kernel<8>);
+    return launch(project_fast_kernel<4>);
+  }
+  // tuning knobs (defaults measured on B200; env overrides are for experiments)
+  const int batch = env_int("MS_GATHER_BATCH", 4);
+  if (batch >= 16) return run_warp_encode(ProjectSource<16>{pos, data, row_offset, pf}, e, status, ticket, err,
+                                          "project_warp", s);
+  if (batch >= 8) return run_warp_encode(ProjectSource<8>{pos, data, row_offset, pf}, e, status, ticket, err,
+                                         "project_warp", s);
+  return run_warp_encode(ProjectSource<4>{pos, data, row_offset, pf}, e, status, ticket, err, "project_warp", s);
+}
+
+}  // namespace ms

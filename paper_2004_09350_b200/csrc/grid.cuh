@@ -1,0 +1,26 @@
+// grid.cuh — launch-configuration helpers shared by libms' translation units.
+#pragma once
+#include <cstdlib>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace ms {
+
+template <class K>
+static inline int persistent_grid(K kernel, int threads, uint64_t items) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t g = (uint64_t)per_sm * num_sms();
+  if (items < g) g = items;
+  return (int)(g ? g : 1);
+}
+
+static inline int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+
+}  // namespace ms

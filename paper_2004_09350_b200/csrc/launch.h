@@ -65,6 +65,11 @@ struct PosEnc {  // output of the warp encoder
 };
 cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                              uint64_t row_offset, uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);
+// positions as DELTA_BP{B <= 512} straight from the mask (posdelta.cuh): widths, scan, pack.
+// Scratch: wk (n_full u32), cwx (n_full + 1 u64), scan status ((n_full + 2047) / 2048 + 1 u64, zeroed), ticket (zeroed).
+cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                                   uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
+                                   uint32_t* scan_ticket, uint32_t* err, cudaStream_t s);
 // project through the warp encoder (positions DELTA_BP with B == G, or O(1) formats; data O(1) formats)
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);

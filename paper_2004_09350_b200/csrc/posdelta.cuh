@@ -1,0 +1,360 @@
+// posdelta.cuh — select's output-side buffer layer for the positions format the
+// paper recommends for select outputs, DELTA_BP ("the output is always
+// sorted"), straight from the select bit mask to the packed column
+// (P:486-490), for block sizes B <= 512.
+//
+// Output block k holds output ranks [kB, kB + B); its first position gstart[k]
+// comes from the segment scan. Three launches, none of which waits on another
+// CTA (a look-back per block or per tile of blocks stalls whole CTAs on their
+// predecessors, measured 3x slower on B200):
+//   pos_width  one warp per block: w_k = ebw(max_j d_j), d_j = p_j - p_{j-1},
+//              d_0 = 0 (D-6);
+//   scan       exclusive prefix of w_k -> cw (D-4), the generic scan kernel;
+//   pos_pack   one warp per block: the same walk, codes streamed into a
+//              shared-memory copy of the block, stored with coalesced 64-bit
+//              stores at word cw[k] * B / 64; cw[k+1], base = p_0 = gstart[k].
+//              The final partial block goes raw to the remainder.
+// Per block the walk is pd_fast_item (mask span <= kPdStageU32 words, i.e.
+// selectivity above ~1.6%: words staged in shared memory, B/32 ranks per lane,
+// equal work per lane, 32-bit relative positions) or, for sparse masks, the
+// round-based walker pd_walk. No position is materialised outside registers.
+#pragma once
+#include "common.cuh"
+#include "launch.h"
+
+namespace ms {
+
+constexpr int kPdWarps = 8;  // warps per CTA (independent)
+constexpr int kPdLaneWords = 8;
+constexpr int kPdRoundWords = 32 * kPdLaneWords;
+constexpr uint32_t kPdStageU32 = 1024;      // mask words staged per warp (also a slow block's pack buffer: 2B u32)
+constexpr uint32_t kPdPackU32 = 16 * 16;    // a fast block: B/32 * w <= 16 * 15 u32
+constexpr uint32_t kPdWarpU32 = kPdStageU32 + kPdPackU32;
+
+// One walk over the mask for output block `item`: ranks [0, cnt) starting at
+// relative row row0. PACK = false: returns the lane's max delta. PACK = true:
+// writes the codes (width w) into buf (zeroed, u32 words), or, when raw !=
+// nullptr, the global positions into raw[rank].
+template <bool PACK>
+__device__ __forceinline__ uint64_t pd_walk(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
+                                            uint32_t cnt, uint32_t w, uint32_t* buf, uint64_t* raw,
+                                            uint64_t row_offset, uint32_t lane, uint32_t* err) {
+  const uint64_t wi = row0 >> 5;
+  const uint32_t fmask = ~0u << (row0 & 31);
+  uint64_t wb = wi & ~3ull;  // 16-byte aligned
+  uint32_t got = 0;
+  uint64_t carry = 0;  // 1 + last position of the previous rounds (0: none)
+  uint64_t maxd = 0;
+  while (got < cnt) {
+    if (wb >= n_words) {  // fewer set bits than the scan counted
+      if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+      break;
+    }
+    const uint64_t wl = wb + (uint64_t)kPdLaneWords * lane;
+    uint32_t x[kPdLaneWords];
+    if (wl + kPdLaneWords <= n_words) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(bits + wl));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(bits + wl) + 1);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kPdLaneWords; ++q) x[q] = wl + q < n_words ? __ldg(bits + wl + q) : 0u;
+    }
+    uint32_t c = 0;
+    uint64_t lastp = 0;
+#pragma unroll
+    for (int q = 0; q < kPdLaneWords; ++q) {
+      const uint64_t m = wl + q;
+      if (m < wi) x[q] = 0;
+      else if (m == wi) x[q] &= fmask;
+      c += __popc(x[q]);
+      if (x[q]) lastp = m * 32 + 32 - __clz(x[q]);
+    }
+    uint32_t inc = c;
+    uint64_t mx = lastp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, inc, o);
+      const uint64_t tm = __shfl_up_sync(kFull, mx, o);
+      if (lane >= (uint32_t)o) {
+        inc += t;
+        mx = tm > mx ? tm : mx;
+      }
+    }
+    const uint32_t total = __shfl_sync(kFull, inc, 31);
+    const uint64_t round_last = __shfl_sync(kFull, mx, 31);
+    uint64_t prev = __shfl_up_sync(kFull, mx, 1);
+    if (lane == 0) prev = 0;
+    prev = prev > carry ? prev : carry;
+    uint32_t k = got + inc - c;
+    if (c && k < cnt) {
+      uint64_t acc = 0;
+      uint32_t nb = 0, widx = 0;
+      bool first = true;
+      if (PACK && !raw) {
+        const uint64_t o = (uint64_t)k * w;
+        widx = (uint32_t)(o >> 5);
+        nb = (uint32_t)(o & 31);
+      }
+      auto flush = [&](uint32_t v) {
+        if (first) {
+          atomicOr(buf + widx, v);
+          first = false;
+        } else {
+          buf[widx] = v;
+        }
+        ++widx;
+      };
+      auto put = [&](uint32_t code, uint32_t cw_) {
+        acc |= (uint64_t)code << nb;
+        nb += cw_;
+        if (nb >= 32) {
+          flush((uint32_t)acc);
+          acc >>= 32;
+          nb -= 32;
+        }
+      };
+#pragma unroll
+      for (int q = 0; q < kPdLaneWords; ++q) {
+        uint32_t word = x[q];
+        const uint64_t rb = (wl + q) * 32;
+        while (word && k < cnt) {
+          const uint32_t bt = __ffs(word) - 1;
+          word &= word - 1;
+          const uint64_t p1 = rb + bt + 1;  // 1 + position
+          const uint64_t d = k ? p1 - prev : 0ull;
+          prev = p1;
+          if (!PACK) {
+            maxd = d > maxd ? d : maxd;
+          } else if (raw) {
+            raw[k] = p1 - 1 + row_offset;
+          } else if (w <= 32) {
+            put((uint32_t)d, w);
+          } else {
+            put((uint32_t)d, 32);
+            put((uint32_t)(d >> 32), w - 32);
+          }
+          ++k;
+        }
+      }
+      if (PACK && !raw && nb) atomicOr(buf + widx, (uint32_t)acc);
+    }
+    got += total;
+    carry = round_last > carry ? round_last : carry;
+    wb += kPdRoundWords;
+  }
+  return maxd;
+}
+
+// Fast block walk, for blocks whose mask span (first word of this block to the
+// word of the next block's first position) fits the stage: lane j owns the
+// PER = B/32 consecutive ranks [PER*j, PER*j + PER).
+//   1. lane j loads C consecutive words [wa + C*j, +C) (16-byte loads), masks
+//      the rows before the block's first position, stages them in shared
+//      memory and counts their set bits; warp exclusive scan -> rank of each
+//      lane's chunk;
+//   2. lane j finds the chunk holding rank PER*j (binary search over the chunk
+//      prefixes by shuffles), walks to its word and bit, then extracts PER
+//      positions in order (32-bit, relative to word wa);
+//   3. d_q = p_q - p_{q-1} (d_0 of lane j from lane j-1's last position, 0
+//      for rank 0). The span bounds every delta by 32 * kPdStageU32 < 2^15.
+// PACK = false: returns w = ebw(max d). PACK = true: streams lane j's codes —
+// the contiguous bit range [PER*j*w, PER*(j+1)*w) — into buf (B*w/32 u32,
+// zeroed here): plain stores inside the range, atomicOr on the two words it
+// may share with its neighbours; returns w.
+template <int PER, bool PACK>
+__device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
+                                                 uint64_t span_words, uint32_t w, uint32_t* stage, uint32_t* buf,
+                                                 uint32_t lane) {
+  const uint64_t wi = row0 >> 5;
+  const uint32_t fmask = ~0u << (row0 & 31);
+  const uint64_t wa = wi & ~3ull;
+  const uint32_t need = (uint32_t)((wi - wa) + span_words);
+  const uint32_t C = ((need + 127) / 128) * 4;  // words per lane, multiple of 4, 32*C >= need
+  const uint32_t wi_rel = (uint32_t)(wi - wa);
+  // 1. stage + count
+  const uint64_t c0 = wa + (uint64_t)C * lane;
+  uint4* st4 = reinterpret_cast<uint4*>(stage) + (C / 4) * lane;
+  uint32_t cnt = 0;
+  for (uint32_t q = 0; q < C; q += 4) {
+    const uint64_t m = c0 + q;
+    uint32_t x0, x1, x2, x3;
+    if (m + 4 <= n_words) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(bits + m));
+      x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w;
+    } else {
+      x0 = m < n_words ? __ldg(bits + m) : 0u;
+      x1 = m + 1 < n_words ? __ldg(bits + m + 1) : 0u;
+      x2 = m + 2 < n_words ? __ldg(bits + m + 2) : 0u;
+      x3 = 0u;
+    }
+    if (m == wa) {  // the first four words hold the block start (wi - wa < 4)
+      x0 = wi_rel > 0 ? 0u : x0 & fmask;
+      x1 = wi_rel > 1 ? 0u : (wi_rel == 1 ? x1 & fmask : x1);
+      x2 = wi_rel > 2 ? 0u : (wi_rel == 2 ? x2 & fmask : x2);
+      x3 = wi_rel == 3 ? x3 & fmask : x3;
+    }
+    st4[q / 4] = make_uint4(x0, x1, x2, x3);
+    cnt += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
+  }
+  __syncwarp();
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, inc, o);
+    if (lane >= (uint32_t)o) inc += t;
+  }
+  const uint32_t ex = inc - cnt;
+  // 2. locate rank PER*j: the last lane L with ex_L <= r
+  const uint32_t r = PER * lane;
+  uint32_t L = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const uint32_t cand = L + step;
+    const uint32_t exc = __shfl_sync(kFull, ex, cand & 31);
+    if (cand < 32 && exc <= r) L = cand;
+  }
+  uint32_t skip = r - __shfl_sync(kFull, ex, L);
+  uint32_t m = C * L;  // staged word index
+  uint32_t cur = stage[m];
+  while (true) {
+    const uint32_t pc = __popc(cur);
+    if (skip < pc) break;
+    skip -= pc;
+    cur = stage[++m];
+  }
+  for (; skip; --skip) cur &= cur - 1;
+  uint32_t pos[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    while (!cur) cur = stage[++m];
+    pos[q] = m * 32 + (__ffs(cur) - 1);
+    cur &= cur - 1;
+  }
+  // 3. deltas
+  const uint32_t prev_last = __shfl_up_sync(kFull, pos[PER - 1], 1);
+  uint32_t d[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) d[q] = q ? pos[q] - pos[q - 1] : (lane ? pos[0] - prev_last : 0u);
+  if (!PACK) {
+    uint32_t mx = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) mx = d[q] > mx ? d[q] : mx;
+    mx = __reduce_max_sync(kFull, mx);
+    return 32 - __clz(mx);
+  }
+  // 4. pack (w <= 15)
+  const uint32_t nw32 = PER * w;  // == B * w / 32
+  for (uint32_t i = lane; i < nw32; i += 32) buf[i] = 0;
+  __syncwarp();
+  if (w) {
+    const uint32_t o = PER * lane * w;
+    uint32_t widx = o >> 5, nb = o & 31;
+    uint32_t acc = 0;
+    bool first = true;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      acc |= d[q] << nb;
+      nb += w;
+      if (nb >= 32) {
+        if (first) {
+          atomicOr(buf + widx, acc);
+          first = false;
+        } else {
+          buf[widx] = acc;
+        }
+        ++widx;
+        nb -= 32;
+        acc = nb ? d[q] >> (w - nb) : 0u;
+      }
+    }
+    if (nb) atomicOr(buf + widx, acc);
+  }
+  __syncwarp();
+  return w;
+}
+
+__device__ __forceinline__ bool pd_span(const uint64_t* gstart, uint64_t item, uint64_t n_items, uint64_t row0,
+                                        uint64_t row_offset, uint64_t* span) {
+  if (item + 1 >= n_items) return false;  // the last block's span is unknown: walker
+  *span = ((__ldg(gstart + item + 1) - row_offset) >> 5) - (row0 >> 5) + 1;
+  return *span + 4 <= kPdStageU32;
+}
+
+// Pass 1: w_k for every full block k < n_full.
+__global__ void __launch_bounds__(kPdWarps * 32) pos_width_kernel(const uint32_t* __restrict__ bits,
+                                                                  uint64_t n_words,
+                                                                  const uint64_t* __restrict__ gstart,
+                                                                  uint64_t row_offset, uint32_t B, uint64_t n_full,
+                                                                  uint64_t n_items, uint32_t* wk, uint32_t* err) {
+  extern __shared__ __align__(16) uint32_t pd_sm[];  // per warp: stage
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* stage = pd_sm + (size_t)wid * kPdStageU32;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
+  for (uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid; item < n_full; item += nwarps) {
+    const uint64_t row0 = __ldg(gstart + item) - row_offset;
+    uint64_t span;
+    uint32_t w;
+    if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
+      w = B == 512   ? pd_fast_item<16, false>(bits, n_words, row0, span, 0, stage, nullptr, lane)
+          : B == 256 ? pd_fast_item<8, false>(bits, n_words, row0, span, 0, stage, nullptr, lane)
+                     : pd_fast_item<4, false>(bits, n_words, row0, span, 0, stage, nullptr, lane);
+      __syncwarp();
+    } else {
+      w = ebw64(warp_max(pd_walk<false>(bits, n_words, row0, B, 0, nullptr, nullptr, row_offset, lane, err)));
+    }
+    if (lane == 0) wk[item] = w;
+  }
+}
+
+// Pass 2: pack every block at cw[k] = cwx[k] (exclusive prefix of the widths).
+__global__ void __launch_bounds__(kPdWarps * 32) pos_pack_kernel(const uint32_t* __restrict__ bits,
+                                                                 uint64_t n_words,
+                                                                 const uint64_t* __restrict__ gstart,
+                                                                 uint64_t row_offset, PosEnc e, uint64_t n_items,
+                                                                 const uint64_t* __restrict__ cwx, uint32_t* err) {
+  extern __shared__ __align__(16) uint32_t pd_sm[];  // per warp: stage | fast pack buffer
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* stage = pd_sm + (size_t)wid * kPdWarpU32;
+  const uint32_t B = e.G;
+  const uint64_t n_full = e.n_out / B;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
+  for (uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid; item < n_items; item += nwarps) {
+    const uint64_t row0 = __ldg(gstart + item) - row_offset;
+    if (item >= n_full) {  // final partial block -> raw remainder
+      pd_walk<true>(bits, n_words, row0, (uint32_t)(e.n_out - item * B), 0, nullptr, e.rem, row_offset, lane, err);
+      continue;
+    }
+    const uint64_t E = __ldg(cwx + item);
+    const uint32_t w = (uint32_t)(__ldg(cwx + item + 1) - E);
+    uint64_t span;
+    const uint32_t* packed;
+    if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
+      uint32_t* buf = stage + kPdStageU32;
+      if (B == 512) pd_fast_item<16, true>(bits, n_words, row0, span, w, stage, buf, lane);
+      else if (B == 256) pd_fast_item<8, true>(bits, n_words, row0, span, w, stage, buf, lane);
+      else pd_fast_item<4, true>(bits, n_words, row0, span, w, stage, buf, lane);
+      packed = buf;
+    } else {
+      const uint32_t nw32 = B / 32 * w;
+      for (uint32_t m = lane; m < nw32; m += 32) stage[m] = 0;
+      __syncwarp();
+      if (w) pd_walk<true>(bits, n_words, row0, B, w, stage, nullptr, row_offset, lane, err);
+      __syncwarp();
+      packed = stage;
+    }
+    if (lane == 0) {
+      if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      e.cw[item + 1] = (uint32_t)(E + w);
+      e.ref[item] = row0 + row_offset;
+    }
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(packed);
+    uint64_t* dst = e.payload + E * (B / 64);
+    const uint32_t nw64 = B / 64 * w;
+    for (uint32_t m = lane; m < nw64; m += 32) dst[m] = src[m];
+    __syncwarp();
+  }
+}
+
+}  // namespace ms

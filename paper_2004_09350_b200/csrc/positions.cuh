@@ -17,12 +17,6 @@
 
 namespace ms {
 
-// select-in-word: position of the (k+1)-th set bit of x (k < popc(x))
-__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
-  for (uint32_t i = 0; i < k; ++i) x &= x - 1;
-  return __ffs(x) - 1;
-}
-
 // Shared-memory tile index with one pad slot every 16 entries: keeps both the
 // lane-consecutive (16 entries per lane) and the lane-strided access patterns
 // of the 8-byte tile free of bank conflicts.
@@ -322,6 +316,136 @@ __global__ void __launch_bounds__(128) warp_encode_kernel(Src src, PosEnc e, uin
     encode_finish<Src>(e, item, P, cnt, w, rmin, status, err, lane);
     __syncwarp();
   }
+}
+
+// Stream lane j's PER codes c[q] (< 2^w, w <= 64) into the u32 words of a
+// block at bits [PER*j*w, PER*(j+1)*w): zero the block's B*w/32 words, then
+// plain stores inside the lane's range and atomicOr on the (at most two) words
+// shared with its neighbours. All 32 lanes call.
+template <int PER>
+__device__ __forceinline__ void pack_lane_codes(uint32_t* buf, const uint64_t (&c)[PER], uint32_t w, uint32_t lane) {
+  const uint32_t nw32 = PER * w;
+  for (uint32_t i = lane; i < nw32; i += 32) buf[i] = 0;
+  __syncwarp();
+  if (w) {
+    const uint32_t o = PER * lane * w;
+    uint32_t widx = o >> 5, nb = o & 31;
+    uint64_t acc = 0;
+    bool first = true;
+    auto flush = [&]() {
+      if (first) {
+        atomicOr(buf + widx, (uint32_t)acc);
+        first = false;
+      } else {
+        buf[widx] = (uint32_t)acc;
+      }
+      ++widx;
+      acc >>= 32;
+      nb -= 32;
+    };
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      if (w <= 32) {
+        acc |= c[q] << nb;
+        nb += w;
+        if (nb >= 32) flush();
+      } else {
+        acc |= (c[q] & 0xffffffffull) << nb;
+        nb += 32;
+        flush();
+        acc |= (c[q] >> 32) << nb;
+        nb += w - 32;
+        if (nb >= 32) flush();
+      }
+    }
+    if (nb) atomicOr(buf + widx, (uint32_t)acc);
+  }
+  __syncwarp();
+}
+
+// Output-side buffer layer with a deferred look-back, one warp per item of
+// G = 32*PER ranks (G <= 512), two tiles per warp: the Source fills the item's
+// values into tile A; lane j takes ranks [PER*j, PER*j + PER) into registers,
+// forms the codes (DELTA: differences, FOR: minus the block minimum, DYN: the
+// values) and the block width, packs the block in place (pack_lane_codes) and
+// publishes the width as its look-back aggregate. Only then does the warp
+// resolve the exclusive width prefix of its PREVIOUS item — whose predecessors
+// have had a whole item's gather to publish — and store that block from tile B
+// with coalesced 64-bit stores at word cw[k] * G / 64. Non-block formats and
+// the final partial block need no prefix and are written directly.
+template <class Src, int PER>
+__global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosEnc e, uint64_t n_items,
+                                                                   uint64_t* status, uint32_t* ticket,
+                                                                   uint32_t* err) {
+  constexpr uint32_t G = 32 * PER;
+  extern __shared__ __align__(16) uint64_t enc_sm[];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t* tiles = enc_sm + (uint64_t)wid * 2 * tile_slots(G);
+  const bool is_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  uint64_t prev = ~0ull, prev_ref = 0;
+  uint32_t prev_w = 0, cur = 0;
+  auto store = [&](uint64_t item, uint32_t w, uint64_t ref, const uint64_t* T) {
+    const uint64_t E = lookback_resolve(status, item, w);
+    if (lane == 0) {
+      if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      e.cw[item + 1] = (uint32_t)(E + w);
+      if (e.format != MS_DYN_BP) e.ref[item] = ref;
+    }
+    uint64_t* dst = e.payload + E * (G / 64);
+    const uint32_t nw64 = G / 64 * w;
+    for (uint32_t m = lane; m < nw64; m += 32) dst[m] = T[m];
+    __syncwarp();
+  };
+  while (true) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(ticket, 1u);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= n_items) break;
+    uint64_t* P = tiles + cur * tile_slots(G);
+    const uint64_t r0 = (uint64_t)item * G;
+    const uint32_t cnt = (uint32_t)min((uint64_t)G, e.n_out - r0);
+    src.load(item, r0, cnt, P, lane, err);
+    if (!is_block || cnt < G) {  // no prefix needed
+      encode_finish<Src>(e, item, P, cnt, 0, 0, status, err, lane);
+      __syncwarp();
+      continue;
+    }
+    uint64_t c[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) c[q] = P[pidx(lane * PER + q)];
+    uint64_t ref = 0, mx = 0;
+    if (e.format == MS_DELTA_BP) {
+      const uint64_t last = __shfl_up_sync(kFull, c[PER - 1], 1);
+      ref = __shfl_sync(kFull, c[0], 0);
+#pragma unroll
+      for (int q = PER - 1; q > 0; --q) c[q] -= c[q - 1];
+      c[0] = lane ? c[0] - last : 0ull;
+    } else if (e.format == MS_FOR_BP) {
+      uint64_t lo = c[0];
+#pragma unroll
+      for (int q = 1; q < PER; ++q) lo = c[q] < lo ? c[q] : lo;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(kFull, lo, o);
+        lo = t < lo ? t : lo;
+      }
+      ref = lo;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) c[q] -= lo;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) mx = c[q] > mx ? c[q] : mx;
+    const uint32_t w = ebw64(warp_max(mx));
+    __syncwarp();
+    pack_lane_codes<PER>(reinterpret_cast<uint32_t*>(P), c, w, lane);
+    lookback_publish(status, item, w);
+    if (prev != ~0ull) store(prev, prev_w, prev_ref, tiles + (cur ^ 1) * tile_slots(G));
+    prev = item;
+    prev_w = w;
+    prev_ref = ref;
+    cur ^= 1;
+  }
+  if (prev != ~0ull) store(prev, prev_w, prev_ref, tiles + (cur ^ 1) * tile_slots(G));
 }
 
 }  // namespace ms

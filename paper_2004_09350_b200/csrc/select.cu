@@ -1,0 +1,257 @@
+// select.cu — select cores (fast compile-time-width core, generic core) and the
+// whole-column sum that reuses the fast core (select_fast.cuh).
+#include "common.cuh"
+#include "engine.cuh"
+#include "grid.cuh"
+#include "select_fast.cuh"
+#include "launch.h"
+
+namespace ms {
+
+// ------------------------------------------------------- select: predicate
+struct RangePred {
+  uint64_t lo, span;
+  uint32_t neg;
+  __device__ __forceinline__ bool operator()(uint64_t v) const { return ((v - lo) <= span) != (neg != 0); }
+};
+struct BitmapPred {
+  const uint64_t* bm;
+  uint64_t bits;
+  __device__ __forceinline__ bool operator()(uint64_t v) const {
+    return v < bits && ((__ldg(bm + (v >> 6)) >> (v & 63)) & 1ull);
+  }
+};
+
+// Generic select core for formats without a fast path (DELTA_BP, RLE, block
+// sizes < 512): per tile of 2048 rows, decode into shared memory, evaluate the
+// predicate, ballot -> one 32-bit mask word per 32 rows; per 512-row segment
+// write count | (1-based last matching row << 16). Only segments in [s0, s1)
+// are written (the fast kernel covers the others).
+template <class Pred>
+__global__ void __launch_bounds__(kThreads) select_generic_kernel(ColView c, Pred pred, uint32_t* bits,
+                                                                  uint32_t* seg_info, uint64_t s0, uint64_t s1) {
+  __shared__ EngineSmem sm;
+  __shared__ uint32_t words[kChunk / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t t0 = (s0 * kSegRows) / kChunk;
+  const uint64_t t1 = (s1 * kSegRows + kChunk - 1) / kChunk;
+  for (uint64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
+    load_rows(c, r0, cnt, sm);
+    constexpr int kWordsPerWarp = kChunk / 32 / (kThreads / 32);
+#pragma unroll
+    for (int q = 0; q < kWordsPerWarp; ++q) {
+      const uint32_t m = wid * kWordsPerWarp + q;
+      const uint32_t i = m * 32 + lane;
+      const bool p = i < cnt && pred(sm.vals[i]);
+      const uint32_t word = __ballot_sync(kFull, p);
+      if (lane == 0) words[m] = word;
+    }
+    __syncthreads();
+    constexpr int kSegsPerTile = kChunk / kSegRows;
+    if (wid < kSegsPerTile) {
+      const uint64_t sg = t * kSegsPerTile + wid;
+      if (sg >= s0 && sg < s1) {
+        const uint32_t my = lane < kSegWords ? words[wid * kSegWords + lane] : 0u;
+        if (lane < kSegWords) bits[sg * kSegWords + lane] = my;
+        const uint32_t cnt_ = (uint32_t)warp_sum(__popc(my));
+        const uint32_t last = (uint32_t)warp_max(my ? lane * 32 + 32 - __clz(my) : 0u);
+        if (lane == 0) seg_info[sg] = cnt_ | (last << 16);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void max_width_kernel(const uint32_t* cw, uint64_t nb, uint32_t* out) {
+  uint32_t m = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride)
+    m = max(m, cw[b + 1] - cw[b]);
+  m = __reduce_max_sync(kFull, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cudaStream_t s) {
+  if (!nb) return cudaSuccess;
+  uint64_t grid = (nb + 255) / 256;
+  if (grid > (uint64_t)num_sms() * 8) grid = num_sms() * 8;
+  ProfScope prof_("max_width", s);
+  max_width_kernel<<<(int)grid, 256, 0, s>>>(cw, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
+                          uint32_t* err, cudaStream_t s) {
+  if (NS == 0) return cudaSuccess;
+  // fast path: UNCOMPR, STATIC_BP, DYN_BP / FOR_BP with B >= 512, on full 512-row segments
+  int kind = -1;
+  uint64_t ns_fast = 0;
+  if (c.format == MS_UNCOMPR) { kind = FAST_UNCOMPR; ns_fast = c.n / kSegRows; }
+  if (c.format == MS_STATIC_BP) { kind = FAST_STATIC; ns_fast = c.n / kSegRows; }
+  if ((c.format == MS_DYN_BP || c.format == MS_FOR_BP) && c.B >= (uint32_t)kSegRows) {
+    kind = FAST_BLOCK;
+    ns_fast = (c.nb << c.log2B) / kSegRows;
+  }
+  if (kind >= 0 && ns_fast) {
+    FastPred fp{p.lo, p.span, p.neg, (uint32_t)p.is_bitmap, p.bitmap, p.bitmap_bits};
+    auto pick = [&](auto k, int stages, int warps_per_cta, int bufu32 = kPairBufWide) {
+      const size_t smem = (size_t)warps_per_cta * stages * bufu32 * 4;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps_per_cta * 32, smem);
+      if (per_sm < 1) per_sm = 1;
+      const uint64_t warps = (uint64_t)per_sm * num_sms() * warps_per_cta;
+      uint64_t spw = (ns_fast + warps - 1) / warps;
+      spw += spw & 1;  // whole segment pairs per warp
+      const uint64_t used = (ns_fast + spw - 1) / spw;
+      const int grid = (int)((used + warps_per_cta - 1) / warps_per_cta);
+      ProfScope prof_("select_fast", s);
+      k<<<grid, warps_per_cta * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw, err, nullptr);
+    };
+    // variants (stages, warps/CTA, min CTAs/SM); default measured on B200, env override for experiments
+    const int v = env_int("MS_SELECT_VARIANT", 0);
+    // narrow staging slots (2 x 2 KiB per pair) when every block is <= 32 bits wide
+    const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
+#define MS_PICK(K)                                                             \
+  do {                                                                         \
+    if (v == 1) pick(select_fast_kernel<K, 3, 4, 2>, 3, 4);                    \
+    else if (v == 2) pick(select_fast_kernel<K, 2, 8, 1>, 2, 8);               \
+    else if (v == 3) pick(select_fast_kernel<K, 3, 4, 4, kPairBufNarrow>, 3, 4, kPairBufNarrow); \
+    else if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow); \
+    else pick(select_fast_kernel<K, 2, 4, 3>, 2, 4);                           \
+  } while (0)
+    if (kind == FAST_UNCOMPR) MS_PICK(FAST_UNCOMPR);
+    else if (kind == FAST_STATIC) MS_PICK(FAST_STATIC);
+    else MS_PICK(FAST_BLOCK);
+#undef MS_PICK
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (ns_fast < NS) {  // the rest (other formats, partial segments, block remainders)
+    const uint64_t tiles = ((NS * kSegRows + kChunk - 1) / kChunk) - (ns_fast * kSegRows) / kChunk;
+    ProfScope prof_("select_generic", s);
+    if (p.is_bitmap) {
+      auto k = select_generic_kernel<BitmapPred>;
+      k<<<persistent_grid(k, kThreads, tiles), kThreads, 0, s>>>(c, BitmapPred{p.bitmap, p.bitmap_bits}, bits,
+                                                                 seg_info, ns_fast, NS);
+    } else {
+      auto k = select_generic_kernel<RangePred>;
+      k<<<persistent_grid(k, kThreads, tiles), kThreads, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits,
+                                                                 seg_info, ns_fast, NS);
+    }
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ sums
+// sum of a whole column mod 2^64, using the format identities:
+// RLE sum v*len; FOR B*ref + sum codes; DELTA B*base + sum (B-j) d_j.
+__global__ void __launch_bounds__(kThreads) sum_kernel(ColView c, unsigned long long* out) {
+  __shared__ uint64_t wsum[kThreads / 32];
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  uint64_t acc = 0;
+  switch (c.format) {
+    case MS_UNCOMPR:
+      for (uint64_t i = gtid; i < c.n; i += gthreads) acc += __ldg(c.payload + i);
+      break;
+    case MS_STATIC_BP:
+      for (uint64_t i = gtid; i < c.n; i += gthreads) acc += unpack_at(c.payload, i * c.w, c.w);
+      break;
+    case MS_RLE:
+      for (uint64_t k = gtid; k < c.nruns; k += gthreads) acc += __ldg(c.payload + 2 * k) * __ldg(c.payload + 2 * k + 1);
+      break;
+    default: {
+      const uint64_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
+      for (uint64_t b = gwarp; b < c.nb; b += gwarps) {
+        const uint32_t cw0 = __ldg(c.cw + b);
+        const uint32_t w = __ldg(c.cw + b + 1) - cw0;
+        const uint64_t bit0 = (uint64_t)cw0 * c.B;
+        uint64_t s = 0;
+        if (w) {
+          for (uint32_t j = lane; j < c.B; j += 32) {
+            const uint64_t code = unpack_at(c.payload, bit0 + (uint64_t)j * w, w);
+            s += c.format == MS_DELTA_BP ? (uint64_t)(c.B - j) * code : code;
+          }
+        }
+        if (lane == 0 && c.format != MS_DYN_BP) s += (uint64_t)c.B * __ldg(c.ref + b);
+        acc += s;
+      }
+      for (uint64_t i = gtid; i < c.nrem; i += gthreads) acc += __ldg(c.rem + i);
+      break;
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int k = 0; k < kThreads / 32; ++k) t += wsum[k];
+    if (t) atomicAdd(out, (unsigned long long)t);
+  }
+}
+
+// rows [r0, n) of a column, one value at a time (the tail the fast scan leaves)
+__global__ void sum_rows_kernel(ColView c, uint64_t r0, unsigned long long* out) {
+  uint64_t acc = 0;
+  for (uint64_t r = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < c.n; r += (uint64_t)gridDim.x * blockDim.x)
+    acc += read_row(c, r);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err, cudaStream_t s) {
+  // fast path: the select scan machinery with a sum core, over full 512-row segments
+  int kind = -1;
+  uint64_t ns_fast = 0;
+  if (c.format == MS_UNCOMPR) { kind = FAST_UNCOMPR; ns_fast = c.n / kSegRows; }
+  if (c.format == MS_STATIC_BP) { kind = FAST_STATIC; ns_fast = c.n / kSegRows; }
+  if ((c.format == MS_DYN_BP || c.format == MS_FOR_BP) && c.B >= (uint32_t)kSegRows) {
+    kind = FAST_BLOCK;
+    ns_fast = (c.nb << c.log2B) / kSegRows;
+  }
+  if (kind < 0 || !ns_fast) {
+    ProfScope prof_("sum", s);
+    sum_kernel<<<persistent_grid(sum_kernel, kThreads, ~0ull), kThreads, 0, s>>>(c, out);
+    return cudaGetLastError();
+  }
+  const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
+  FastPred fp{};
+  auto pick = [&](auto k, int bufu32) {
+    const size_t smem = (size_t)4 * 2 * bufu32 * 4;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 4 * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t warps = (uint64_t)per_sm * num_sms() * 4;
+    uint64_t spw = (ns_fast + warps - 1) / warps;
+    spw += spw & 1;
+    const uint64_t used = (ns_fast + spw - 1) / spw;
+    const int grid = (int)((used + 3) / 4);
+    ProfScope prof_("sum_fast", s);
+    k<<<grid, 4 * 32, smem, s>>>(c, fp, nullptr, nullptr, ns_fast, spw, err, out);
+  };
+#define MS_PICK_SUM(K)                                                                               \
+  do {                                                                                               \
+    if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow, CORE_SUM>, kPairBufNarrow);      \
+    else pick(select_fast_kernel<K, 2, 4, 3, kPairBufWide, CORE_SUM>, kPairBufWide);                 \
+  } while (0)
+  if (kind == FAST_UNCOMPR) MS_PICK_SUM(FAST_UNCOMPR);
+  else if (kind == FAST_STATIC) MS_PICK_SUM(FAST_STATIC);
+  else MS_PICK_SUM(FAST_BLOCK);
+#undef MS_PICK_SUM
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const uint64_t r0 = ns_fast * kSegRows;
+  if (r0 < c.n) {
+    ProfScope prof_("sum_tail", s);
+    sum_rows_kernel<<<8, 256, 0, s>>>(c, r0, out);
+  }
+  return cudaGetLastError();
+}
+
+// sum of data at positions (select -> project -> sum fused)
+}  // namespace ms

@@ -1,0 +1,85 @@
+"""GPU parity of project's register-resident path (project.cuh: DELTA_BP{G}
+positions -> DYN_BP / FOR_BP data -> block output of size G or UNCOMPR)
+against the oracle, bit-exact: densities that do and do not fit the 32-block
+data window, data blocks wider than 32 bits, unsorted and repeated positions,
+positions in the data remainder, a final partial positions block, and the
+range error."""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.gpu_util import assert_same_image, get_ms, oracle_fmt, to_torch
+
+pytestmark = pytest.mark.gpu
+
+# the encoder paths project can take for these inputs (env switches read at launch)
+PATHS = {"default": {}, "fast_source": {"MS_PROJECT_FAST": "1"}, "regs": {"MS_PROJECT_REGS": "1"}}
+
+
+@pytest.fixture(params=sorted(PATHS))
+def path(request, monkeypatch):
+    for k, v in PATHS[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+def _data(rng, n, kind):
+    if kind == "narrow":
+        return (np.uint64(10**6) + rng.integers(0, 1 << 20, n).astype(np.uint64))
+    if kind == "mixed":  # some blocks wider than 32 bits
+        v = rng.integers(0, 1 << 12, n).astype(np.uint64)
+        hot = rng.random(n) < 0.002
+        v[hot] = rng.integers(1 << 40, 1 << 63, int(hot.sum()), dtype=np.uint64)
+        return v
+    return rng.integers(0, 2**64 - 1, n, dtype=np.uint64, endpoint=True)  # wide
+
+
+@pytest.mark.parametrize("kind", ["narrow", "mixed", "wide"])
+@pytest.mark.parametrize("density", [0.5, 0.0625, 0.004])
+def test_project_fast(kind, density, path):
+    ms = get_ms()
+    rng = np.random.default_rng(hash((kind, density)) & 0xffff)
+    n = 300_001
+    off = 7_000_000_000
+    v = _data(rng, n, kind)
+    sel = np.nonzero(rng.random(n) < density)[0].astype(np.uint64) + np.uint64(off)
+    for fd in (ms.for_bp(512), ms.dyn_bp(512), ms.for_bp(128), ms.dyn_bp(2048)):
+        gd = ms.compress(to_torch(v), fd)
+        od = O.encode(v, *oracle_fmt(fd))
+        for G in (512, 128):
+            fp = ms.delta_bp(G)
+            gp = ms.compress(to_torch(sel), fp)
+            op_ = O.encode(sel, *oracle_fmt(fp))
+            outs = [ms.for_bp(G), ms.delta_bp(G), ms.dyn_bp(G)] + ([ms.uncompr()] if G == 512 else [])
+            for fo in outs:
+                gr = ms.project(gd, gp, off, fo)
+                orr = O.project(od, op_, off, *oracle_fmt(fo))
+                assert_same_image(gr, orr, f"project {kind} d={density} {fd} @ DELTA_BP{{{G}}} -> {fo}")
+
+
+def test_project_fast_unsorted_and_repeated(path):
+    ms = get_ms()
+    rng = np.random.default_rng(11)
+    n = 100_000
+    v = _data(rng, n, "narrow")
+    pos = np.sort(rng.integers(0, n, 20_000)).astype(np.uint64)   # repeated positions
+    pos[1000:1600] = rng.integers(0, n, 600).astype(np.uint64)    # an unsorted stretch
+    pos[-5:] = np.uint64(n - 1)                                     # the data remainder
+    gd = ms.compress(to_torch(v), ms.for_bp(512))
+    od = O.encode(v, O.FOR_BP, 0, 512)
+    gp = ms.compress(to_torch(pos), ms.delta_bp(512))
+    op_ = O.encode(pos, O.DELTA_BP, 0, 512)
+    for fo in (ms.for_bp(512), ms.uncompr(), ms.delta_bp(512)):
+        assert_same_image(ms.project(gd, gp, 0, fo), O.project(od, op_, 0, *oracle_fmt(fo)), f"-> {fo}")
+
+
+def test_project_fast_range_error(path):
+    ms = get_ms()
+    v = np.arange(5000, dtype=np.uint64)
+    gd = ms.compress(to_torch(v), ms.for_bp(512))
+    pos = np.arange(0, 1024, dtype=np.uint64) * 4
+    pos[700] = 5000  # one past the end
+    gp = ms.compress(to_torch(np.sort(pos)), ms.delta_bp(512))
+    with pytest.raises(ms.MsError) as e:
+        ms.project(gd, gp, 0, ms.for_bp(512))
+    assert e.value.code == 4  # MS_E_RANGE
