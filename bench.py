@@ -249,10 +249,12 @@ def run_ours(args):
     total_sel = sum(counts)
     gsum = ms.u64(s)
     parity = {"selected": total_sel, "sum": gsum}
-    if args.n_log2 == 32:
-        parity["expected_selected"] = 268_436_914
-        parity["expected_sum"] = 409_182_112_845_958
-        parity["ok"] = total_sel == 268_436_914 and gsum == 409_182_112_845_958
+    apath = os.path.join(ROOT, "tests", "golden", "config_anchors.json")  # written by tools/make_anchors.py (oracle)
+    if args.n_log2 == 32 and os.path.exists(apath):
+        a5 = json.load(open(apath))["c5"]
+        parity["expected_selected"] = a5["count"]
+        parity["expected_sum"] = a5["sum_projected"]
+        parity["ok"] = total_sel == a5["count"] and gsum == a5["sum_projected"]
         if not parity["ok"]:
             print(json.dumps({"error": "parity failure", "parity": parity}), flush=True)
             return 1
@@ -299,6 +301,8 @@ def run_ours(args):
            "pos_pack": mask_bytes + bytes_pos,                     # mask read, positions image written
            "pos_encode": mask_bytes + bytes_pos,
            "project_fast": gather_bytes + bytes_yp,                # positions + touched Y + Y' written
+           "project_pipe": gather_bytes + bytes_yp,
+           "project_win": gather_bytes + bytes_yp,
            "project_warp": gather_bytes + bytes_yp,
            "sum_fast": bytes_yp}                                   # Y' read
     kernels = {}

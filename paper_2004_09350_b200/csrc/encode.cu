@@ -5,6 +5,7 @@
 #include "positions.cuh"
 #include "posdelta.cuh"
 #include "project.cuh"
+#include "projwin.cuh"
 #include "launch.h"
 
 namespace ms {
@@ -99,37 +100,64 @@ cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_
   const bool out_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
   const uint32_t pf = (uint32_t)env_int("MS_GATHER_PREFETCH", 1);
   if (pos.format == MS_DELTA_BP && pos.B == e.G && e.G >= 128 && e.G <= 512 &&
-      (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && env_int("MS_PROJECT_FAST", 0)) {
-    if (e.G == 512) return run_warp_encode(ProjectFastSource<16>{pos, data, row_offset, pf}, e, status, ticket, err,
-                                           "project_fast", s);
-    if (e.G == 256) return run_warp_encode(ProjectFastSource<8>{pos, data, row_offset, pf}, e, status, ticket, err,
-                                           "project_fast", s);
-    return run_warp_encode(ProjectFastSource<4>{pos, data, row_offset, pf}, e, status, ticket, err, "project_fast", s);
+      (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && (out_block || e.format == MS_UNCOMPR) &&
+      env_int("MS_PROJECT_WIN", 0)) {
+    const uint64_t n_full = e.n_out / e.G;
+    if (n_full) {
+      auto launch = [&](auto k) {
+        const size_t smem = 2 * (size_t)kWinSlotBytes + 3 * (size_t)tile_slots(e.G) * 8;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem);
+        if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
+        if (per_sm < 1) per_sm = 1;
+        uint64_t grid = (uint64_t)per_sm * num_sms();
+        if (n_full < grid) grid = n_full;
+        ProfScope prof_("project_win", s);
+        k<<<(int)grid, 32, smem, s>>>(pos, data, row_offset, e, n_full, status, err);
+        return cudaGetLastError();
+      };
+      cudaError_t r = e.G == 512   ? launch(project_win_kernel<16>)
+                      : e.G == 256 ? launch(project_win_kernel<8>)
+                                   : launch(project_win_kernel<4>);
+      if (r != cudaSuccess) return r;
+    }
+    if (n_full * e.G < e.n_out) {
+      ProfScope prof_("project_tail", s);
+      project_tail_kernel<<<1, 256, 0, s>>>(pos, data, row_offset, e, n_full * e.G, err);
+    }
+    return cudaGetLastError();
   }
   if (pos.format == MS_DELTA_BP && pos.B == e.G && e.G >= 128 && e.G <= 512 &&
       (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && (out_block || e.format == MS_UNCOMPR) &&
-      env_int("MS_PROJECT_REGS", 0)) {
-    const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
-    if (!n_items) return cudaSuccess;
-    auto launch = [&](auto k) {
-      const int warps = 4;
-      const size_t smem = (size_t)warps * 2 * (2 * e.G) * 4;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
-  if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
-      if (per_sm < 1) per_sm = 1;
-      uint64_t grid = (uint64_t)per_sm * num_sms();
-      const uint64_t need = (n_items + warps - 1) / warps;
-      if (need < grid) grid = need;
-      ProfScope prof_("project_regs", s);
-      k<<<(int)grid, warps * 32, smem, s>>>(pos, data, row_offset, e, n_items, status, ticket, err,
-                                            (uint32_t)env_int("MS_GATHER_PREFETCH", 1));
-      return cudaGetLastError();
-    };
-    if (e.G == 512) return launch(project_fast_kernel<16>);
-    if (e.G == 256) return launch(project_fast_kernel<8>);
-    return launch(project_fast_kernel<4>);
+      env_int("MS_PROJECT_PIPE", 0)) {
+    const uint64_t n_full = e.n_out / e.G;
+    if (n_full) {
+      auto launch = [&](auto k) {
+        const int warps = 4;
+        const size_t smem = (size_t)warps * 3 * tile_slots(e.G) * 8;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+        if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
+        if (per_sm < 1) per_sm = 1;
+        uint64_t grid = (uint64_t)per_sm * num_sms();
+        const uint64_t need = (n_full + warps - 1) / warps;
+        if (need < grid) grid = need;
+        ProfScope prof_("project_pipe", s);
+        k<<<(int)grid, warps * 32, smem, s>>>(pos, data, row_offset, e, n_full, status, err, pf);
+        return cudaGetLastError();
+      };
+      cudaError_t r = e.G == 512   ? launch(project_pipe_kernel<16>)
+                      : e.G == 256 ? launch(project_pipe_kernel<8>)
+                                   : launch(project_pipe_kernel<4>);
+      if (r != cudaSuccess) return r;
+    }
+    if (n_full * e.G < e.n_out) {
+      ProfScope prof_("project_tail", s);
+      project_tail_kernel<<<1, 256, 0, s>>>(pos, data, row_offset, e, n_full * e.G, err);
+    }
+    return cudaGetLastError();
   }
   // tuning knobs (defaults measured on B200; env overrides are for experiments)
   const int batch = env_int("MS_GATHER_BATCH", 4);

@@ -8,6 +8,7 @@
 // with warp ballot + popc into one 32-bit mask word per 32 rows.
 #pragma once
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ms {
 
@@ -55,38 +56,6 @@ __device__ __forceinline__ void code_interval(uint64_t lo, uint64_t span, uint32
     const uint64_t chi = (d - 1) < M1 ? (d - 1) : M1;
     a = (uint32_t)(e + 1); s = (uint32_t)(chi - (e + 1)); neg = neg0 ^ 1u;
   }
-}
-
-// ---- TMA bulk copy + mbarrier helpers (sm_90+; SASS UBLKCP / SYNCS)
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(count));
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          (uint32_t)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra LAB_WAIT;\n"
-      "}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
 }
 
 // ---- lane-consecutive core: lane l of a half-warp owns rows 32l .. 32l+31 of

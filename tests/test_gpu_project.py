@@ -13,7 +13,8 @@ from tests.gpu_util import assert_same_image, get_ms, oracle_fmt, to_torch
 pytestmark = pytest.mark.gpu
 
 # the encoder paths project can take for these inputs (env switches read at launch)
-PATHS = {"default": {}, "fast_source": {"MS_PROJECT_FAST": "1"}, "regs": {"MS_PROJECT_REGS": "1"}}
+PATHS = {"default": {}, "pipe": {"MS_PROJECT_PIPE": "1"}, "ticketed": {"MS_ENCODE_TICKET": "1"},
+         "window": {"MS_PROJECT_WIN": "1"}}
 
 
 @pytest.fixture(params=sorted(PATHS))
