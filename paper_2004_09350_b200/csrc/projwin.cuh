@@ -160,12 +160,34 @@ __global__ void __launch_bounds__(32) project_win_kernel(ColView pos, ColView da
 
   auto decode = [&](uint64_t it, uint64_t* T) {
     const uint32_t cw0 = __ldg(pos.cw + it), wp = __ldg(pos.cw + it + 1) - cw0;
+    const uint64_t bref = __ldg(pos.ref + it);
     const uint64_t bit0 = (uint64_t)cw0 * G + (uint64_t)PER * lane * wp;
     uint64_t acc = 0;
     uint64_t p[PER];
     if (wp == 0) {
 #pragma unroll
       for (int q = 0; q < PER; ++q) p[q] = 0;
+    } else if (wp <= 8 && PER == 16) {  // the lane's <= 128 + 31 bits: five loads issued together
+      const uint32_t* w32 = reinterpret_cast<const uint32_t*>(pos.payload) + (bit0 >> 5);
+      const uint32_t sft = (uint32_t)(bit0 & 31), nwd = (sft + PER * wp + 31) >> 5;
+      const uint32_t x0 = __ldg(w32), x1 = nwd > 1 ? __ldg(w32 + 1) : 0u, x2 = nwd > 2 ? __ldg(w32 + 2) : 0u,
+                     x3 = nwd > 3 ? __ldg(w32 + 3) : 0u, x4 = nwd > 4 ? __ldg(w32 + 4) : 0u;
+      uint64_t win = ((uint64_t)x1 << 32 | x0) >> sft;
+      uint32_t avail = 64 - sft, k = 2;
+      const uint64_t m = (1ull << wp) - 1;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        if (avail < wp) {
+          const uint32_t nx = k == 2 ? x2 : (k == 3 ? x3 : x4);
+          win |= (uint64_t)nx << avail;
+          avail += 32;
+          ++k;
+        }
+        acc += win & m;
+        p[q] = acc;
+        win >>= wp;
+        avail -= wp;
+      }
     } else if (wp <= 32) {
       BitReader br;
       br.init(pos.payload, bit0);
@@ -182,7 +204,7 @@ __global__ void __launch_bounds__(32) project_win_kernel(ColView pos, ColView da
       }
     }
     const uint64_t incl = warp_incl_scan(acc);
-    const uint64_t base = __ldg(pos.ref + it) + incl - acc;
+    const uint64_t base = bref + incl - acc;
 #pragma unroll
     for (int q = 0; q < PER; ++q) T[pidx(PER * lane + q)] = p[q] + base;
     __syncwarp();
