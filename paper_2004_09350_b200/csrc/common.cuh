@@ -133,7 +133,7 @@ constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull <<
 // in flight), spins only on the ones not yet published, and stops at the first
 // inclusive prefix (flag P) in descending item order. The window width sets how
 // fast the P frontier can advance (128 items per L2 round trip).
-__device__ __forceinline__ uint64_t lookback_walk(const uint64_t* status, uint64_t t) {
+__device__ __forceinline__ uint64_t lookback_walk(uint64_t* status, uint64_t t) {
   const int lane = threadIdx.x & 31;
   uint64_t excl = 0;
   int64_t base = (int64_t)t - 1;
@@ -165,7 +165,8 @@ __device__ __forceinline__ uint64_t lookback_walk(const uint64_t* status, uint64
     if (pmask) break;
     base -= 128;
   }
-  return excl & kValMask;
+  excl &= kValMask;
+  return excl;
 }
 
 // Call with ALL 32 lanes of ONE warp. Returns the exclusive prefix of item t.

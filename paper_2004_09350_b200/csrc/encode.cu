@@ -12,8 +12,10 @@ namespace ms {
 
 // ------------------------------------------------- select output encoder
 template <class Src>
-static cudaError_t run_warp_encode(const Src& src, const PosEnc& e, uint64_t* status, uint32_t* ticket,
+static cudaError_t run_warp_encode(const Src& src, const PosEnc& e0, uint64_t* status, uint32_t* ticket,
                                    uint32_t* err, const char* name, cudaStream_t s) {
+  PosEnc e = e0;
+  e.exp = (uint32_t)env_int("MS_EXP", 0);
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   if (!n_items) return cudaSuccess;
   if (e.G <= 512 && !env_int("MS_ENCODE_TICKET", 0)) {  // deferred look-back, two tiles per warp

@@ -94,9 +94,33 @@ struct ProjectSource {
       const uint64_t bit0 = (uint64_t)cw0 * pos.B;
       const uint32_t per = pos.B / 32;  // consecutive codes per lane
       uint64_t acc = 0;
-      for (uint32_t q = 0; q < per; ++q) {
-        acc += unpack_at(pos.payload, bit0 + (uint64_t)(lane * per + q) * w, w);
-        P[pidx(lane * per + q)] = acc;
+      if (per == 16 && w >= 1 && w <= 8) {  // the lane's <= 128 + 31 bits: five loads issued together
+        const uint64_t lb = bit0 + (uint64_t)lane * 16 * w;
+        const uint32_t* w32 = reinterpret_cast<const uint32_t*>(pos.payload) + (lb >> 5);
+        const uint32_t sft = (uint32_t)(lb & 31), nwd = (sft + 16 * w + 31) >> 5;
+        const uint32_t x0 = __ldg(w32), x1 = nwd > 1 ? __ldg(w32 + 1) : 0u, x2 = nwd > 2 ? __ldg(w32 + 2) : 0u,
+                       x3 = nwd > 3 ? __ldg(w32 + 3) : 0u, x4 = nwd > 4 ? __ldg(w32 + 4) : 0u;
+        uint64_t win = ((uint64_t)x1 << 32 | x0) >> sft;
+        uint32_t avail = 64 - sft, k = 2;
+        const uint64_t m = (1ull << w) - 1;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (avail < w) {
+            const uint32_t nx = k == 2 ? x2 : (k == 3 ? x3 : x4);
+            win |= (uint64_t)nx << avail;
+            avail += 32;
+            ++k;
+          }
+          acc += win & m;
+          P[pidx(lane * 16 + q)] = acc;
+          win >>= w;
+          avail -= w;
+        }
+      } else {
+        for (uint32_t q = 0; q < per; ++q) {
+          acc += unpack_at(pos.payload, bit0 + (uint64_t)(lane * per + q) * w, w);
+          P[pidx(lane * per + q)] = acc;
+        }
       }
       uint64_t incl = warp_incl_scan(acc);
       const uint64_t base = __ldg(pos.ref + b) + incl - acc;
@@ -385,7 +409,7 @@ __global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosE
   uint64_t prev = ~0ull, prev_ref = 0;
   uint32_t prev_w = 0, cur = 0;
   auto store = [&](uint64_t item, uint32_t w, uint64_t ref, const uint64_t* T) {
-    const uint64_t E = lookback_resolve(status, item, w);
+    const uint64_t E = (e.exp & 2) ? item * w : lookback_resolve(status, item, w);  // bit 1: experiment
     if (lane == 0) {
       if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
       e.cw[item + 1] = (uint32_t)(E + w);
@@ -404,7 +428,7 @@ __global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosE
     uint64_t* P = tiles + cur * tile_slots(G);
     const uint64_t r0 = (uint64_t)item * G;
     const uint32_t cnt = (uint32_t)min((uint64_t)G, e.n_out - r0);
-    src.load(item, r0, cnt, P, lane, err);
+    if (!(e.exp & 1)) src.load(item, r0, cnt, P, lane, err);  // bit 0: experiment, no source
     if (!is_block || cnt < G) {  // no prefix needed
       encode_finish<Src>(e, item, P, cnt, 0, 0, status, err, lane);
       __syncwarp();
