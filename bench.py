@@ -301,6 +301,8 @@ def run_ours(args):
            "pos_width": mask_bytes,                                # mask read
            "pos_pack": mask_bytes + bytes_pos,                     # mask read, positions image written
            "pos_encode": mask_bytes + bytes_pos,
+           "pos_slot": mask_bytes + bytes_pos,                     # mask read, blocks written to slots
+           "pos_copy": 2 * bytes_pos,                              # slots read, positions image written
            "project_fast": gather_bytes + bytes_yp,                # positions + touched Y + Y' written
            "project_pipe": gather_bytes + bytes_yp,
            "project_win": gather_bytes + bytes_yp,

@@ -2,6 +2,7 @@
 // (P:469, 477-479): validates descriptors, splits columns into main part and
 // remainder (by descriptor), sizes and allocates outputs, launches the
 // kernels and performs the op's single read-back synchronisation.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -43,6 +44,12 @@ struct Ctx {
     else cudaFreeAsync(p, s);
   }
 };
+
+// experiment switches (measured alternatives; defaults are the measured-best paths)
+bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
 
 // One scratch allocation per op, carved into 256-byte aligned regions.
 struct Scratch {
@@ -667,13 +674,24 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
     pe.cw = out->cw;
     pe.ref = out->ref;
     pe.rem = out->rem;
+    // single-walk slots for DELTA_BP positions: every delta is < NS * 512 rows, so
+    // wcap = ebw(NS * 512 - 1) bits per code bound every block (B * wcap / 64 words per slot)
+    uint64_t* slots = nullptr;
+    uint32_t slot_words = 0;
+    if (pos_delta && f.format == MS_DELTA_BP && !env_flag("MS_POS_TWO_WALKS")) {
+      const uint32_t wcap = ebw_host(NS * kSegRows - 1);
+      slot_words = G / 64 * (wcap ? wcap : 1);
+      slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
+      if (!slots) { release(ctx, out); return MS_E_NOMEM; }
+    }
     cudaError_t e =
         pos_delta && f.format == MS_DELTA_BP
             ? launch_positions_delta(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
                                      sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
-                                     sc.at<uint32_t>(o_tk3), err, ctx.s)
+                                     sc.at<uint32_t>(o_tk3), slots, slot_words, err, ctx.s)
             : launch_positions(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
                                sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
+    ctx.free(slots);  // stream-ordered free: the copy kernel is queued before it
     if (e != cudaSuccess) {
       release(ctx, out);
       return cuda_status(e);

@@ -62,7 +62,8 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
 
 cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                                    uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
-                                   uint32_t* scan_ticket, uint32_t* err, cudaStream_t s) {
+                                   uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* err,
+                                   cudaStream_t s) {
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   const uint64_t n_full = e.n_out / e.G;
   if (!n_items) return cudaSuccess;
@@ -76,6 +77,24 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
     const uint64_t need = (items + kPdWarps - 1) / kPdWarps;
     return (int)(need < g ? (need ? need : 1) : g);
   };
+  if (slots && n_full) {  // single walk: slots, scan, copy
+    const size_t smem = (size_t)kPdWarps * kPdWarpU32 * 4;
+    const int grid = grid_for(pos_slot_kernel, smem, n_items);
+    {
+      ProfScope prof_("pos_slot", s);
+      pos_slot_kernel<<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items, slots,
+                                                         slot_words, wk, err);
+    }
+    cudaError_t r = cudaGetLastError();
+    if (r != cudaSuccess) return r;
+    r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
+    if (r != cudaSuccess) return r;
+    uint64_t cgrid = (n_full + 7) / 8;
+    if (cgrid > (uint64_t)num_sms() * 8) cgrid = num_sms() * 8;
+    ProfScope prof_("pos_copy", s);
+    pos_copy_kernel<<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
+    return cudaGetLastError();
+  }
   if (n_full) {
     const size_t smem = (size_t)kPdWarps * kPdStageU32 * 4;
     const int grid = grid_for(pos_width_kernel, smem, n_full);

@@ -68,9 +68,12 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
                              uint64_t row_offset, uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);
 // positions as DELTA_BP{B <= 512} straight from the mask (posdelta.cuh): widths, scan, pack.
 // Scratch: wk (n_full u32), cwx (n_full + 1 u64), scan status ((n_full + 2047) / 2048 + 1 u64, zeroed), ticket (zeroed).
+// slots != nullptr: single walk into per-block slots of slot_words u64 (n_full slots), then scan + copy;
+// else two walks (widths, scan, pack).
 cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                                    uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
-                                   uint32_t* scan_ticket, uint32_t* err, cudaStream_t s);
+                                   uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* err,
+                                   cudaStream_t s);
 // project through the warp encoder (positions DELTA_BP with B == G, or O(1) formats; data O(1) formats)
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);

@@ -160,10 +160,11 @@ __device__ __forceinline__ uint64_t pd_walk(const uint32_t* __restrict__ bits, u
 //   3. d_q = p_q - p_{q-1} (d_0 of lane j from lane j-1's last position, 0
 //      for rank 0). The span bounds every delta by 32 * kPdStageU32 < 2^15.
 // PACK = false: returns w = ebw(max d). PACK = true: streams lane j's codes —
+// (AUTO_W: at the width it computes; else at the given w) —
 // the contiguous bit range [PER*j*w, PER*(j+1)*w) — into buf (B*w/32 u32,
 // zeroed here): plain stores inside the range, atomicOr on the two words it
 // may share with its neighbours; returns w.
-template <int PER, bool PACK>
+template <int PER, bool PACK, bool AUTO_W = false>
 __device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
                                                  uint64_t span_words, uint32_t w, uint32_t* stage, uint32_t* buf,
                                                  uint32_t lane) {
@@ -237,12 +238,13 @@ __device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bi
   uint32_t d[PER];
 #pragma unroll
   for (int q = 0; q < PER; ++q) d[q] = q ? pos[q] - pos[q - 1] : (lane ? pos[0] - prev_last : 0u);
-  if (!PACK) {
+  if (!PACK || AUTO_W) {
     uint32_t mx = 0;
 #pragma unroll
     for (int q = 0; q < PER; ++q) mx = d[q] > mx ? d[q] : mx;
     mx = __reduce_max_sync(kFull, mx);
-    return 32 - __clz(mx);
+    w = 32 - __clz(mx);
+    if (!PACK) return w;
   }
   // 4. pack (w <= 15)
   const uint32_t nw32 = PER * w;  // == B * w / 32
@@ -354,6 +356,87 @@ __global__ void __launch_bounds__(kPdWarps * 32) pos_pack_kernel(const uint32_t*
     const uint32_t nw64 = B / 64 * w;
     for (uint32_t m = lane; m < nw64; m += 32) dst[m] = src[m];
     __syncwarp();
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Single-walk variant (the default): pos_slot packs every full block at its own
+// width into a fixed-size slot (B * wcap bits, wcap = ebw(rows - 1) bounds
+// every delta) and records w_k and the base; the generic scan turns the widths
+// into cw; pos_copy moves each block from its slot to word cw[k] * B / 64. The
+// extra traffic (slots written and read back, ~2 x the positions image) costs
+// less than a second walk of the mask.
+__global__ void __launch_bounds__(kPdWarps * 32) pos_slot_kernel(const uint32_t* __restrict__ bits,
+                                                                 uint64_t n_words,
+                                                                 const uint64_t* __restrict__ gstart,
+                                                                 uint64_t row_offset, PosEnc e, uint64_t n_items,
+                                                                 uint64_t* __restrict__ slots, uint32_t slot_words,
+                                                                 uint32_t* __restrict__ wk, uint32_t* err) {
+  extern __shared__ __align__(16) uint32_t pd_sm[];  // per warp: stage | fast pack buffer
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* stage = pd_sm + (size_t)wid * kPdWarpU32;
+  const uint32_t B = e.G;
+  const uint64_t n_full = e.n_out / B;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
+  for (uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid; item < n_items; item += nwarps) {
+    const uint64_t row0 = __ldg(gstart + item) - row_offset;
+    if (item >= n_full) {  // final partial block -> raw remainder
+      pd_walk<true>(bits, n_words, row0, (uint32_t)(e.n_out - item * B), 0, nullptr, e.rem, row_offset, lane, err);
+      continue;
+    }
+    uint64_t span;
+    uint32_t w;
+    const uint32_t* packed;
+    if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
+      uint32_t* buf = stage + kPdStageU32;
+      w = B == 512   ? pd_fast_item<16, true, true>(bits, n_words, row0, span, 0, stage, buf, lane)
+          : B == 256 ? pd_fast_item<8, true, true>(bits, n_words, row0, span, 0, stage, buf, lane)
+                     : pd_fast_item<4, true, true>(bits, n_words, row0, span, 0, stage, buf, lane);
+      packed = buf;
+    } else {
+      w = ebw64(warp_max(pd_walk<false>(bits, n_words, row0, B, 0, nullptr, nullptr, row_offset, lane, err)));
+      const uint32_t nw32 = B / 32 * w;
+      for (uint32_t m = lane; m < nw32; m += 32) stage[m] = 0;
+      __syncwarp();
+      if (w) pd_walk<true>(bits, n_words, row0, B, w, stage, nullptr, row_offset, lane, err);
+      __syncwarp();
+      packed = stage;
+    }
+    const uint32_t nw64 = B / 64 * w;
+    if (nw64 > slot_words) {  // cannot happen: wcap bounds every delta
+      if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+    } else {
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(packed);
+      uint64_t* dst = slots + item * slot_words;
+      for (uint32_t m = lane; m < nw64; m += 32) dst[m] = src[m];
+    }
+    if (lane == 0) {
+      wk[item] = w;
+      e.ref[item] = row0 + row_offset;
+    }
+    __syncwarp();
+  }
+}
+
+// one warp per block: slot -> payload at cw[k] * B / 64 (16-byte copies), cw[k+1]
+__global__ void __launch_bounds__(256) pos_copy_kernel(PosEnc e, uint64_t n_full, const uint64_t* __restrict__ slots,
+                                                       uint32_t slot_words, const uint64_t* __restrict__ cwx,
+                                                       uint32_t* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t item = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < n_full;
+       item += nwarps) {
+    const uint64_t E = __ldg(cwx + item);
+    const uint32_t w = (uint32_t)(__ldg(cwx + item + 1) - E);
+    if (lane == 0) {
+      if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      e.cw[item + 1] = (uint32_t)(E + w);
+    }
+    const uint32_t n2 = e.G / 128 * w;  // 16-byte units (B*w/64 words, B >= 128)
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(slots + item * slot_words);
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(e.payload + E * (e.G / 64));
+    for (uint32_t m = lane; m < n2; m += 32) dst[m] = __ldg(src + m);
   }
 }
 

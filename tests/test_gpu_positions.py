@@ -13,8 +13,17 @@ pytestmark = pytest.mark.gpu
 SELECTIVITY = [1.0, 0.9, 0.5, 0.0625, 0.02, 0.0155, 0.005, 0.0003]
 
 
+@pytest.fixture(params=["slots", "two_walks"])
+def walk(request, monkeypatch):
+    """Both encoder pipelines: single walk into slots + copy (default), or
+    width walk + pack walk (MS_POS_TWO_WALKS=1)."""
+    if request.param == "two_walks":
+        monkeypatch.setenv("MS_POS_TWO_WALKS", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("sel", SELECTIVITY)
-def test_positions_delta_bp(sel):
+def test_positions_delta_bp(sel, walk):
     ms = get_ms()
     rng = np.random.default_rng(int(sel * 1e6) + 7)
     for n in (600_001, 512 * 1024):
@@ -29,7 +38,7 @@ def test_positions_delta_bp(sel):
                 assert_same_image(g, o, f"sel={sel} n={n} B={B} off={off}")
 
 
-def test_positions_clustered():
+def test_positions_clustered(walk):
     """Matches in dense clusters separated by long gaps: blocks mix both paths
     within one CTA tile."""
     ms = get_ms()
