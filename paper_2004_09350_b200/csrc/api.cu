@@ -720,6 +720,10 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
   const uint64_t o_st = sc.add(8 * (items + 1), true);
   const uint64_t o_tk = sc.add(8, true);
   const uint64_t o_tk2 = sc.add(8, true);
+  const uint64_t o_wk = sc.add(4 * (items + 1), false);
+  const uint64_t o_cwx = sc.add(8 * (items + 2), false);
+  const uint64_t o_st3 = sc.add(8 * ((items + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk3 = sc.add(8, true);
   RlePrep rp_pos, rp_data;
   plan_rle(sc, positions, rp_pos);
   plan_rle(sc, data, rp_data);
@@ -759,8 +763,27 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
     pe.cw = out->cw;
     pe.ref = out->ref;
     pe.rem = out->rem;
+    // per-block slots (no look-back) for block outputs of size <= 512 and UNCOMPR; the
+    // slot holds a block at the largest width its codes can have
+    const bool slotted = G <= 512 && (is_block(f.format) || f.format == MS_UNCOMPR) &&
+                         !env_flag("MS_PROJECT_DEFERRED") && !env_flag("MS_PROJECT_PIPE") &&
+                         !env_flag("MS_PROJECT_WIN") && !env_flag("MS_ENCODE_TICKET");
+    uint64_t* slots = nullptr;
+    uint32_t slot_words = 0;
+    if (slotted && is_block(f.format) && n / G) {
+      uint32_t wcap = 64;
+      if (df == MS_STATIC_BP && f.format != MS_DELTA_BP) wcap = data->fmt.bit_width ? data->fmt.bit_width : 64;
+      slot_words = G / 64 * wcap;
+      slots = (uint64_t*)ctx.alloc(8 * (n / G) * (uint64_t)slot_words);
+      if (!slots) e = cudaErrorMemoryAllocation;
+    }
     if (e == cudaSuccess)
-      e = launch_project_warp(pv, dv, row_offset, pe, sc.at<uint64_t>(o_st), sc.at<uint32_t>(o_tk), err, ctx.s);
+      e = slotted ? launch_project_slots(pv, dv, row_offset, pe, slots, slot_words, sc.at<uint32_t>(o_wk),
+                                         sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3), sc.at<uint32_t>(o_tk3), err,
+                                         ctx.s)
+                  : launch_project_warp(pv, dv, row_offset, pe, sc.at<uint64_t>(o_st), sc.at<uint32_t>(o_tk), err,
+                                        ctx.s);
+    ctx.free(slots);
     if (e != cudaSuccess) {
       release(ctx, out);
       return cuda_status(e);

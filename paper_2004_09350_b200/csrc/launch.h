@@ -78,6 +78,12 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);
 
+// project into per-block slots (G <= 512, block formats or UNCOMPR), scan of the widths, copy.
+// Scratch: slots (n/G * slot_words u64), wk (n/G u32), cwx (n/G + 1 u64), scan status (zeroed), ticket (zeroed).
+cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
+                                 uint64_t* slots, uint32_t slot_words, uint32_t* wk, uint64_t* cwx,
+                                 uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err, cudaStream_t s);
+
 // RLE run starts (exclusive prefix of lengths), validation against n
 cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
                               uint32_t* ticket, uint32_t* err, cudaStream_t s);

@@ -472,4 +472,72 @@ __global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosE
   if (prev != ~0ull) store(prev, prev_w, prev_ref, tiles + (cur ^ 1) * tile_slots(G));
 }
 
+// Slot variant of the output-side buffer layer (no look-back at all): one tile
+// per warp, items in grid-stride order; a full block is packed at its own width
+// and written to its fixed-size slot (slot_words u64), its width to wk[k] and its
+// reference to ref[k]; the scan of wk gives cw, and pos_copy_kernel moves each
+// block to word cw[k] * G / 64. Non-block formats and the final partial block
+// are written directly.
+template <class Src, int PER>
+__global__ void __launch_bounds__(128) warp_encode_slot_kernel(Src src, PosEnc e, uint64_t n_items,
+                                                               uint64_t* __restrict__ slots, uint32_t slot_words,
+                                                               uint32_t* __restrict__ wk, uint32_t* err) {
+  constexpr uint32_t G = 32 * PER;
+  extern __shared__ __align__(16) uint64_t enc_sm[];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t* P = enc_sm + (uint64_t)wid * tile_slots(G);
+  const bool is_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  const uint64_t NW = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t item = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid; item < n_items; item += NW) {
+    const uint64_t r0 = item * G;
+    const uint32_t cnt = (uint32_t)min((uint64_t)G, e.n_out - r0);
+    src.load((uint32_t)item, r0, cnt, P, lane, err);
+    if (!is_block || cnt < G) {
+      encode_finish<Src>(e, (uint32_t)item, P, cnt, 0, 0, nullptr, err, lane);
+      __syncwarp();
+      continue;
+    }
+    uint64_t c[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) c[q] = P[pidx(lane * PER + q)];
+    uint64_t ref = 0, mx = 0;
+    if (e.format == MS_DELTA_BP) {
+      const uint64_t last = __shfl_up_sync(kFull, c[PER - 1], 1);
+      ref = __shfl_sync(kFull, c[0], 0);
+#pragma unroll
+      for (int q = PER - 1; q > 0; --q) c[q] -= c[q - 1];
+      c[0] = lane ? c[0] - last : 0ull;
+    } else if (e.format == MS_FOR_BP) {
+      uint64_t lo = c[0];
+#pragma unroll
+      for (int q = 1; q < PER; ++q) lo = c[q] < lo ? c[q] : lo;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(kFull, lo, o);
+        lo = t < lo ? t : lo;
+      }
+      ref = lo;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) c[q] -= lo;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) mx = c[q] > mx ? c[q] : mx;
+    const uint32_t w = ebw64(warp_max(mx));
+    __syncwarp();
+    pack_lane_codes<PER>(reinterpret_cast<uint32_t*>(P), c, w, lane);
+    const uint32_t nw64 = G / 64 * w;
+    if (nw64 > slot_words) {  // a width above the host's bound (an understated hint)
+      if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+    } else {
+      uint64_t* dst = slots + item * slot_words;
+      for (uint32_t m = lane; m < nw64; m += 32) dst[m] = P[m];
+    }
+    if (lane == 0) {
+      wk[item] = w;
+      if (e.format != MS_DYN_BP) e.ref[item] = ref;
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace ms

@@ -13,8 +13,8 @@ from tests.gpu_util import assert_same_image, get_ms, oracle_fmt, to_torch
 pytestmark = pytest.mark.gpu
 
 # the encoder paths project can take for these inputs (env switches read at launch)
-PATHS = {"default": {}, "pipe": {"MS_PROJECT_PIPE": "1"}, "ticketed": {"MS_ENCODE_TICKET": "1"},
-         "window": {"MS_PROJECT_WIN": "1"}}
+PATHS = {"default": {}, "deferred": {"MS_PROJECT_DEFERRED": "1"}, "pipe": {"MS_PROJECT_PIPE": "1"},
+         "ticketed": {"MS_ENCODE_TICKET": "1"}, "window": {"MS_PROJECT_WIN": "1"}}
 
 
 @pytest.fixture(params=sorted(PATHS))
