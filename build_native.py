@@ -100,14 +100,36 @@ def build_libms(force=False):
         _run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart"])
 
 
+def build_shim(force=False):
+    """paper_2004_09350_b200/libms_torchalloc.so: ms_ctx alloc/free callbacks into
+    PyTorch's CUDA caching allocator (g++, torch headers; plumbing, no compute)."""
+    import sysconfig  # noqa: F401
+    try:
+        import torch
+    except Exception:  # torch missing: the binding falls back to ctypes callbacks
+        return
+    pkg = os.path.join(ROOT, "paper_2004_09350_b200")
+    src = os.path.join(pkg, "csrc", "shim", "torch_alloc.cpp")
+    so = os.path.join(pkg, "libms_torchalloc.so")
+    if not (force or _stale(so, [src])):
+        return
+    tdir = os.path.dirname(torch.__file__)
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", f"-D_GLIBCXX_USE_CXX11_ABI={abi}",
+          "-I", os.path.join(tdir, "include"), "-I", "/usr/local/cuda/include", src, "-o", so,
+          "-L", os.path.join(tdir, "lib"), "-lc10", "-lc10_cuda", "-Wl,-rpath," + os.path.join(tdir, "lib")])
+
+
 def build_all(force=False):
     build_synth(force)
     build_oracle(force)
     build_libms(force)
+    build_shim(force)
 
 
 if __name__ == "__main__":
     what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["all"]
     force = "--force" in sys.argv
     for w in what:
-        {"synth": build_synth, "oracle": build_oracle, "libms": build_libms, "all": build_all}[w](force)
+        {"synth": build_synth, "oracle": build_oracle, "libms": build_libms, "shim": build_shim,
+         "all": build_all}[w](force)

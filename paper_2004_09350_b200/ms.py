@@ -143,10 +143,29 @@ def _torch_free(_ctx, ptr, _stream):
         torch.cuda.caching_allocator_delete(int(ptr))
 
 
+_SHIM = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libms_torchalloc.so")
+_native_alloc = None
+
+
+def _alloc_fns():
+    """(alloc, free) for ms_ctx: the native shim into PyTorch's caching allocator
+    (csrc/shim/torch_alloc.cpp, no Python per allocation) when built, else the
+    ctypes callbacks above. Allocation plumbing only; no compute."""
+    global _native_alloc
+    if _native_alloc is None:
+        if os.path.exists(_SHIM):
+            shim = ctypes.CDLL(_SHIM)
+            _native_alloc = (shim, ctypes.cast(shim.ms_torch_alloc, _ALLOC_FN), ctypes.cast(shim.ms_torch_free, _FREE_FN))
+        else:
+            _native_alloc = (None, _torch_alloc, _torch_free)
+    return _native_alloc[1], _native_alloc[2]
+
+
 def _ctx(stream: Optional[torch.cuda.Stream] = None, flags: int = 0) -> _Ctx:
     if stream is None:
         stream = torch.cuda.current_stream()
-    return _Ctx(stream=stream.cuda_stream, alloc=_torch_alloc, free=_torch_free, alloc_ctx=None, flags=flags)
+    a, f = _alloc_fns()
+    return _Ctx(stream=stream.cuda_stream, alloc=a, free=f, alloc_ctx=None, flags=flags)
 
 
 def _check(rc: int, where: str):
