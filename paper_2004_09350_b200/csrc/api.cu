@@ -600,13 +600,13 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] 1 + max position
   const uint64_t o_bits = sc.add(4 * n_words, false);
   const uint64_t o_seg = sc.add(4 * (NS + 1), false);
-  const uint64_t o_off = sc.add(8 * (NS + 1), true);
+  const uint64_t o_off = sc.add(8 * (NS + 1), false);  // the scan writes every entry
   const uint64_t o_gs = sc.add(8 * (items_max + 1), false);
   const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
   const uint64_t o_tk1 = sc.add(8, true);
-  const uint64_t o_st2 = sc.add(8 * (items_max + 1), true);
-  const uint64_t o_tk2 = sc.add(8, true);
   const bool pos_delta = out_fmt.format == MS_DELTA_BP && G <= 512;  // posdelta.cuh
+  const uint64_t o_st2 = sc.add(pos_delta ? 8 : 8 * (items_max + 1), true);  // look-back status (other formats)
+  const uint64_t o_tk2 = sc.add(8, true);
   const uint64_t o_wk = pos_delta ? sc.add(4 * (items_max + 1), false) : 0;
   const uint64_t o_cwx = pos_delta ? sc.add(8 * (items_max + 2), false) : 0;
   const uint64_t o_st3 = pos_delta ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
@@ -715,9 +715,19 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
   const uint64_t n = positions->n;
   if (is_block(out_fmt.format) && 64 * (n / out_fmt.block_size) > 0xffffffffull) return MS_E_INVALID;
   const uint64_t items = (n + 127) / 128;  // enough for any item size (>= 128 rows)
+  // the slot path (no look-back status) serves item sizes <= 512 into block formats or UNCOMPR
+  const uint32_t G0 = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;
+  const int32_t pf0 = positions->fmt.format, df0 = data->fmt.format;
+  const bool warp_path = (pf0 == MS_UNCOMPR || pf0 == MS_STATIC_BP || pf0 == MS_DYN_BP || pf0 == MS_FOR_BP ||
+                          (pf0 == MS_DELTA_BP && positions->fmt.block_size == G0)) &&
+                         (df0 == MS_UNCOMPR || df0 == MS_STATIC_BP || df0 == MS_DYN_BP || df0 == MS_FOR_BP) &&
+                         !(out_fmt.format == MS_STATIC_BP && out_fmt.bit_width == 0);
+  const bool slot_path = warp_path && G0 <= 512 && (is_block(out_fmt.format) || out_fmt.format == MS_UNCOMPR) &&
+                         !env_flag("MS_PROJECT_DEFERRED") && !env_flag("MS_PROJECT_PIPE") &&
+                         !env_flag("MS_PROJECT_WIN") && !env_flag("MS_ENCODE_TICKET");
   Scratch sc(ctx);
   const uint64_t o_meta = sc.add(64, true);
-  const uint64_t o_st = sc.add(8 * (items + 1), true);
+  const uint64_t o_st = sc.add(slot_path ? 8 : 8 * (items + 1), true);
   const uint64_t o_tk = sc.add(8, true);
   const uint64_t o_tk2 = sc.add(8, true);
   const uint64_t o_wk = sc.add(4 * (items + 1), false);
@@ -765,9 +775,7 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
     pe.rem = out->rem;
     // per-block slots (no look-back) for block outputs of size <= 512 and UNCOMPR; the
     // slot holds a block at the largest width its codes can have
-    const bool slotted = G <= 512 && (is_block(f.format) || f.format == MS_UNCOMPR) &&
-                         !env_flag("MS_PROJECT_DEFERRED") && !env_flag("MS_PROJECT_PIPE") &&
-                         !env_flag("MS_PROJECT_WIN") && !env_flag("MS_ENCODE_TICKET");
+    const bool slotted = slot_path;
     uint64_t* slots = nullptr;
     uint32_t slot_words = 0;
     if (slotted && is_block(f.format) && n / G) {
