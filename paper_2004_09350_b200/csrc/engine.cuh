@@ -27,6 +27,11 @@ struct OutView {
   uint64_t* status;          // look-back status, one per item
   uint32_t* ticket;
   unsigned long long* max_out;  // OUT_MAX_ONLY target
+  // slot mode (block formats): tile k's blocks are packed into slots[k * kChunk ...]
+  // (64 bits per row bounds every width), their widths go to bw[block]; the host
+  // scans bw into cw and tile_copy_kernel moves every tile to its place — no look-back
+  uint64_t* slots;
+  uint32_t* bw;
 };
 
 // Output word m (bits [64m, 64m+64)) of a packed stream of `cnt` codes of width
@@ -119,11 +124,15 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     }
     const uint64_t incl = warp_incl_scan(w);
     const uint64_t tile_sum = __shfl_sync(kFull, incl, 31);
-    const uint64_t E = lookback_warp(o.status, item, tile_sum);
+    const uint64_t E = o.slots ? 0ull : lookback_warp(o.status, item, tile_sum);
     if (lane < (int)nbc) {
       const uint64_t c_incl = E + incl;
-      if (c_incl > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
-      o.cw[kb0 + lane + 1] = (uint32_t)c_incl;
+      if (o.slots) {
+        o.bw[kb0 + lane] = w;
+      } else {
+        if (c_incl > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+        o.cw[kb0 + lane + 1] = (uint32_t)c_incl;
+      }
       sm.bex[lane] = E + incl - w;
       if (o.format == MS_FOR_BP) o.ref[kb0 + lane] = sm.bmin[lane];
       if (o.format == MS_DELTA_BP) o.ref[kb0 + lane] = sm.vals[lane << lg];
@@ -135,23 +144,46 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     const uint32_t w = sm.bw[bi];
     if (w == 0) continue;
     const uint64_t* v = sm.vals + (bi << lg);
+    uint64_t* const dst = o.slots ? o.slots + (uint64_t)item * kChunk : o.payload;  // tile slot or final place
     const uint64_t wbase = sm.bex[bi] * (B / 64);
     const uint32_t nwords = (B / 64) * w;
     if (o.format == MS_FOR_BP) {
       const uint64_t rf = sm.bmin[bi];
       auto code = [&](uint32_t j) { return v[j] - rf; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, B, w, m);
+      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m);
     } else if (o.format == MS_DELTA_BP) {
       auto code = [&](uint32_t j) { return j ? v[j] - v[j - 1] : 0ull; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, B, w, m);
+      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m);
     } else {
       auto code = [&](uint32_t j) { return v[j]; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, B, w, m);
+      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m);
     }
   }
   const uint32_t rem_cnt = cnt - (nbc << lg);
   if (rem_cnt) {  // the final partial block -> uncompressed remainder
     for (uint32_t i = tid; i < rem_cnt; i += kThreads) o.rem[i] = sm.vals[(nbc << lg) + i];
+  }
+}
+
+// slot mode, second half: tile k's packed blocks (slot words [0, (cwx[kb1] - cwx[kb0]) * B / 64))
+// -> payload word cwx[kb0] * B / 64, and cw[b + 1] = cwx[b + 1] for its blocks. One CTA per tile.
+static __global__ void __launch_bounds__(256) tile_copy_kernel(OutView o, uint64_t n_tiles, uint64_t nb, const uint64_t* cwx,
+                                                        uint32_t* err) {
+  const uint32_t per = kChunk >> o.log2B;  // blocks per full tile
+  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint64_t kb0 = t * per;
+    if (kb0 >= nb) break;
+    const uint64_t kb1 = min(kb0 + per, nb);
+    const uint64_t E = cwx[kb0];
+    const uint64_t words = (cwx[kb1] - E) * (o.B / 64);
+    for (uint64_t b = kb0 + threadIdx.x; b < kb1; b += blockDim.x) {
+      if (cwx[b + 1] > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      o.cw[b + 1] = (uint32_t)cwx[b + 1];
+    }
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(o.slots + t * kChunk);
+    uint64_t* dst = o.payload + E * (o.B / 64);
+    // B >= 128: the tile's words start 16-byte aligned on both sides (B/64 * w words, B/64 even)
+    for (uint64_t m = threadIdx.x; m < words / 2; m += blockDim.x) reinterpret_cast<ulonglong2*>(dst)[m] = src[m];
   }
 }
 

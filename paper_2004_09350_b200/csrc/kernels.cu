@@ -134,6 +134,16 @@ cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64
   return cudaGetLastError();
 }
 
+cudaError_t launch_tile_copy(const OutView& o, uint64_t n_tiles, uint64_t nb, const uint64_t* cwx, uint32_t* err,
+                             cudaStream_t s) {
+  if (!n_tiles || !nb) return cudaSuccess;
+  uint64_t g = n_tiles;
+  if (g > (uint64_t)num_sms() * 16) g = num_sms() * 16;
+  ProfScope prof_("tile_copy", s);
+  tile_copy_kernel<<<(int)g, 256, 0, s>>>(o, n_tiles, nb, cwx, err);
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------- generic scan
 // Exclusive prefix over N values in one pass (decoupled look-back); epi(idx,
 // exclusive, value) consumes each entry, epi_total(total) is called once.
@@ -385,17 +395,57 @@ cudaError_t launch_rle_len(const uint64_t* starts, uint64_t R, uint64_t n, uint6
 __global__ void __launch_bounds__(kThreads) sum_at_kernel(ColView data, ColView pos, uint64_t row_offset,
                                                           unsigned long long* out, uint32_t* err) {
   __shared__ EngineSmem sm;
+  __shared__ EngineSmem dsm;  // decoded data tile (sequential formats)
   __shared__ uint64_t wsum[kThreads / 32];
+  __shared__ unsigned long long s_lo, s_hi;
   const uint64_t T = (pos.n + kChunk - 1) / kChunk;
+  // DELTA_BP / RLE data have no O(1) random access (D-12): when a chunk's positions
+  // span few data tiles, decode those tiles once (load_rows) and pick the values
+  // from shared memory instead of one O(B) / O(log R) read_row per position
+  const bool seq = data.format == MS_DELTA_BP || data.format == MS_RLE;
   uint64_t acc = 0;
   for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
     const uint64_t r0 = t * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, pos.n - r0);
     load_rows(pos, r0, cnt, sm);
-    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-      const uint64_t p = sm.vals[i];
-      if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
-      else acc += read_row(data, p - row_offset);
+    bool tiled = false;
+    if (seq) {
+      if (threadIdx.x == 0) {
+        s_lo = ~0ull;
+        s_hi = 0;
+      }
+      __syncthreads();
+      unsigned long long lo = ~0ull, hi = 0;
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+        const uint64_t p = sm.vals[i];
+        lo = p < lo ? p : lo;
+        hi = p > hi ? p : hi;
+      }
+      atomicMin(&s_lo, lo);
+      atomicMax(&s_hi, hi);
+      __syncthreads();
+      const uint64_t plo = s_lo, phi = s_hi;
+      tiled = plo >= row_offset && phi - row_offset < data.n && (phi - plo) < 4ull * kChunk;
+      if (tiled) {
+        const uint64_t t_lo = (plo - row_offset) / kChunk, t_hi = (phi - row_offset) / kChunk;
+        for (uint64_t dt = t_lo; dt <= t_hi; ++dt) {
+          const uint64_t d0 = dt * kChunk;
+          const uint32_t dcnt = (uint32_t)min((uint64_t)kChunk, data.n - d0);
+          load_rows(data, d0, dcnt, dsm);  // ends with a barrier
+          for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+            const uint64_t r = sm.vals[i] - row_offset;
+            if (r >= d0 && r < d0 + dcnt) acc += dsm.vals[r - d0];
+          }
+          __syncthreads();
+        }
+      }
+    }
+    if (!tiled) {
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+        const uint64_t p = sm.vals[i];
+        if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
+        else acc += read_row(data, p - row_offset);
+      }
     }
     __syncthreads();
   }

@@ -44,6 +44,9 @@ cudaError_t launch_engine_bitmask(const uint32_t* bits, const uint64_t* tile_off
 cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64_t row_offset, const OutView& out,
                                  uint32_t* err, cudaStream_t s);
 
+// engine slot mode: tiles' packed blocks (OutView.slots) -> payload at the scanned cw (cwx, nb + 1 entries)
+cudaError_t launch_tile_copy(const OutView& o, uint64_t n_tiles, uint64_t nb, const uint64_t* cwx, uint32_t* err,
+                             cudaStream_t s);
 // select core: bit mask (16 words per 512-row segment) + seg_info (count | last << 16)
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
                           uint32_t* err, cudaStream_t s);

@@ -9,10 +9,28 @@
 namespace ms {
 
 // ------------------------------------------------------- select: predicate
+// Header-only block decisions (the specialized-operator shortcut of P:352,
+// SURVEY.md §8(f) #1): a block whose values are known from its header alone to
+// lie in [L, H] needs no decoding when the predicate is constant on [L, H].
+enum : uint32_t { kDecode = 0, kNone = 1, kAll = 2 };
+__device__ __forceinline__ uint32_t range_decision(uint64_t lo, uint64_t span, uint32_t neg, uint64_t L, uint64_t H) {
+  const uint64_t xl = L - lo, xh = H - lo;  // keep(v) <=> (v - lo) <= span, != neg
+  uint32_t d = kDecode;
+  if (xl <= xh) {  // [L, H] maps to [xl, xh] without wrapping
+    if (xh <= span) d = kAll;
+    else if (xl > span) d = kNone;
+  } else if (span == ~0ull) {
+    d = kAll;
+  }
+  if (d != kDecode && neg) d = kAll + kNone - d;
+  return d;
+}
+
 struct RangePred {
   uint64_t lo, span;
   uint32_t neg;
   __device__ __forceinline__ bool operator()(uint64_t v) const { return ((v - lo) <= span) != (neg != 0); }
+  __device__ __forceinline__ uint32_t decide(uint64_t L, uint64_t H) const { return range_decision(lo, span, neg, L, H); }
 };
 struct BitmapPred {
   const uint64_t* bm;
@@ -20,7 +38,41 @@ struct BitmapPred {
   __device__ __forceinline__ bool operator()(uint64_t v) const {
     return v < bits && ((__ldg(bm + (v >> 6)) >> (v & 63)) & 1ull);
   }
+  __device__ __forceinline__ uint32_t decide(uint64_t, uint64_t) const { return kDecode; }
 };
+
+// Header-only decision for a whole 2048-row tile of a block format (all blocks of
+// the tile in the main part): the tile is decided when every block's value range,
+// known from its header alone, gets the same constant verdict. DYN_BP: [0, 2^w);
+// FOR_BP: [ref, ref + 2^w); DELTA_BP: [base, base + (B - 1)(2^w - 1)] (deltas are
+// unsigned; valid when that bound does not overflow).
+template <class Pred>
+__device__ __forceinline__ uint32_t tile_decision(const ColView& c, const Pred& pred, uint64_t r0, uint32_t cnt) {
+  if (c.format != MS_DYN_BP && c.format != MS_FOR_BP && c.format != MS_DELTA_BP) return kDecode;
+  if (cnt != (uint32_t)kChunk || r0 + kChunk > (c.nb << c.log2B)) return kDecode;
+  uint32_t verdict = kDecode;
+  for (uint64_t b = r0 >> c.log2B; b < (r0 + kChunk) >> c.log2B; ++b) {
+    const uint32_t w = __ldg(c.cw + b + 1) - __ldg(c.cw + b);
+    if (w > 64) return kDecode;
+    const uint64_t M1 = w >= 64 ? ~0ull : ((1ull << w) - 1);
+    uint64_t L = 0, H = M1;
+    if (c.format == MS_FOR_BP) {
+      L = __ldg(c.ref + b);
+      H = L + M1;
+      if (H < L) return kDecode;
+    } else if (c.format == MS_DELTA_BP) {
+      L = __ldg(c.ref + b);
+      const uint64_t steps = (uint64_t)(c.B - 1);
+      if (M1 && __umul64hi(M1, steps)) return kDecode;
+      H = L + M1 * steps;
+      if (H < L) return kDecode;
+    }
+    const uint32_t d = pred.decide(L, H);
+    if (d == kDecode || (verdict != kDecode && d != verdict)) return kDecode;
+    verdict = d;
+  }
+  return verdict;
+}
 
 // Generic select core for formats without a fast path (DELTA_BP, RLE, block
 // sizes < 512): per tile of 2048 rows, decode into shared memory, evaluate the
@@ -35,18 +87,26 @@ __global__ void __launch_bounds__(kThreads) select_generic_kernel(ColView c, Pre
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t t0 = (s0 * kSegRows) / kChunk;
   const uint64_t t1 = (s1 * kSegRows + kChunk - 1) / kChunk;
+  __shared__ uint32_t s_dec;
   for (uint64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
     const uint64_t r0 = t * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
-    load_rows(c, r0, cnt, sm);
+    if (threadIdx.x == 0) s_dec = tile_decision(c, pred, r0, cnt);
+    __syncthreads();
+    const uint32_t dec = s_dec;
     constexpr int kWordsPerWarp = kChunk / 32 / (kThreads / 32);
+    if (dec != kDecode) {  // decided from the headers: no decoding
+      if (lane < kWordsPerWarp) words[wid * kWordsPerWarp + lane] = dec == kAll ? 0xffffffffu : 0u;
+    } else {
+      load_rows(c, r0, cnt, sm);
 #pragma unroll
-    for (int q = 0; q < kWordsPerWarp; ++q) {
-      const uint32_t m = wid * kWordsPerWarp + q;
-      const uint32_t i = m * 32 + lane;
-      const bool p = i < cnt && pred(sm.vals[i]);
-      const uint32_t word = __ballot_sync(kFull, p);
-      if (lane == 0) words[m] = word;
+      for (int q = 0; q < kWordsPerWarp; ++q) {
+        const uint32_t m = wid * kWordsPerWarp + q;
+        const uint32_t i = m * 32 + lane;
+        const bool p = i < cnt && pred(sm.vals[i]);
+        const uint32_t word = __ballot_sync(kFull, p);
+        if (lane == 0) words[m] = word;
+      }
     }
     __syncthreads();
     constexpr int kSegsPerTile = kChunk / kSegRows;
@@ -82,9 +142,69 @@ cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cud
   return cudaGetLastError();
 }
 
+// RLE: the predicate is evaluated once per run (P:163's per-run view of
+// the column); a matching run sets its row range in the mask — whole 32-bit words
+// by plain stores, the (at most two) partial words by atomicOr — and the
+// per-segment counts follow from the mask.
+template <class Pred>
+__global__ void __launch_bounds__(256) rle_mask_kernel(ColView c, Pred pred, uint32_t* bits) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < c.nruns; k += stride) {
+    if (!pred(__ldg(c.payload + 2 * k))) continue;
+    const uint64_t a = __ldg(c.run_starts + k), e = __ldg(c.run_starts + k + 1);  // rows [a, e)
+    if (a >= e) continue;
+    const uint64_t wa = a >> 5, we = (e - 1) >> 5;
+    const uint32_t ma = ~0u << (a & 31), me = ~0u >> (31 - ((e - 1) & 31));
+    if (wa == we) {
+      atomicOr(bits + wa, ma & me);
+    } else {
+      atomicOr(bits + wa, ma);
+      for (uint64_t q = wa + 1; q < we; ++q) bits[q] = ~0u;
+      atomicOr(bits + we, me);
+    }
+  }
+}
+
+// per 512-row segment: count | (1-based last matching row << 16), from the mask
+__global__ void __launch_bounds__(256) seg_info_kernel(const uint32_t* bits, uint64_t NS, uint32_t* seg_info) {
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t sg2 = gw; sg2 * 2 < NS; sg2 += nw) {  // a warp takes two segments (32 words)
+    const uint64_t sg = sg2 * 2 + (lane >> 4);
+    const uint32_t m = sg < NS ? bits[sg * kSegWords + (lane & 15)] : 0u;
+    uint32_t cnt = __popc(m);
+    uint32_t last = m ? (lane & 15) * 32 + 32 - __clz(m) : 0u;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      cnt += __shfl_xor_sync(kFull, cnt, o);
+      last = max(last, __shfl_xor_sync(kFull, last, o));
+    }
+    if (sg < NS && (lane & 15) == 0) seg_info[sg] = cnt | (last << 16);
+  }
+}
+
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
                           uint32_t* err, cudaStream_t s) {
   if (NS == 0) return cudaSuccess;
+  if (c.format == MS_RLE && c.run_starts) {
+    cudaError_t e = cudaMemsetAsync(bits, 0, 4 * NS * kSegWords, s);
+    if (e != cudaSuccess) return e;
+    uint64_t g = (c.nruns + 255) / 256;
+    if (g > (uint64_t)num_sms() * 16) g = num_sms() * 16;
+    if (g) {
+      ProfScope prof_("select_rle", s);
+      if (p.is_bitmap) rle_mask_kernel<<<(int)g, 256, 0, s>>>(c, BitmapPred{p.bitmap, p.bitmap_bits}, bits);
+      else rle_mask_kernel<<<(int)g, 256, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    uint64_t g2 = (NS + 15) / 16;
+    if (g2 > (uint64_t)num_sms() * 16) g2 = num_sms() * 16;
+    ProfScope prof_("seg_info", s);
+    seg_info_kernel<<<(int)g2, 256, 0, s>>>(bits, NS, seg_info);
+    return cudaGetLastError();
+  }
   // fast path: UNCOMPR, STATIC_BP, DYN_BP / FOR_BP with B >= 512, on full 512-row segments
   int kind = -1;
   uint64_t ns_fast = 0;
