@@ -757,7 +757,8 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
                           (pf0 == MS_DELTA_BP && positions->fmt.block_size == G0)) &&
                          (df0 == MS_UNCOMPR || df0 == MS_STATIC_BP || df0 == MS_DYN_BP || df0 == MS_FOR_BP) &&
                          !(out_fmt.format == MS_STATIC_BP && out_fmt.bit_width == 0);
-  const bool slot_path = warp_path && G0 <= 512 && (is_block(out_fmt.format) || out_fmt.format == MS_UNCOMPR) &&
+  const bool slot_path = warp_path && G0 <= 512 &&
+                         (is_block(out_fmt.format) || out_fmt.format == MS_UNCOMPR || out_fmt.format == MS_STATIC_BP) &&
                          !env_flag("MS_PROJECT_DEFERRED") && !env_flag("MS_PROJECT_PIPE") &&
                          !env_flag("MS_PROJECT_WIN") && !env_flag("MS_ENCODE_TICKET");
   Scratch sc(ctx);

@@ -195,6 +195,45 @@ __device__ __forceinline__ uint64_t lookback_resolve(uint64_t* status, uint64_t 
   return excl;
 }
 
+// Stream N codes c[q] (< 2^w, w <= 64) into u32 words `buf` at bits
+// [bit0, bit0 + N*w) — the caller's contiguous range: plain stores for the words
+// inside it, atomicOr for the (at most two) words it may share with the
+// neighbouring ranges. `buf` must be zeroed; the caller synchronises.
+template <int N>
+__device__ __forceinline__ void stream_codes(uint32_t* buf, const uint64_t (&c)[N], uint32_t w, uint32_t bit0) {
+  if (!w) return;
+  uint32_t widx = bit0 >> 5, nb = bit0 & 31;
+  uint64_t acc = 0;
+  bool first = true;
+  auto flush = [&]() {
+    if (first) {
+      atomicOr(buf + widx, (uint32_t)acc);
+      first = false;
+    } else {
+      buf[widx] = (uint32_t)acc;
+    }
+    ++widx;
+    acc >>= 32;
+    nb -= 32;
+  };
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    if (w <= 32) {
+      acc |= c[q] << nb;
+      nb += w;
+      if (nb >= 32) flush();
+    } else {
+      acc |= (c[q] & 0xffffffffull) << nb;
+      nb += 32;
+      flush();
+      acc |= (c[q] >> 32) << nb;
+      nb += w - 32;
+      if (nb >= 32) flush();
+    }
+  }
+  if (nb) atomicOr(buf + widx, (uint32_t)acc);
+}
+
 // floor(x / w) for x < 2^20, 1 <= w <= 64, given magic = 0xffffffff / w + 1
 // (computed once per block): a multiply-high plus one correction step
 __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, uint32_t magic) {

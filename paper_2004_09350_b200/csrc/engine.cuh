@@ -275,12 +275,62 @@ struct GatherSource {
         if (i < cnt) sm.vals[i] = rf[q] + v;
       }
     } else {
-      for (uint32_t i = tid; i < cnt; i += kThreads) {
-        const uint64_t p = sm.vals[i];
-        uint64_t v = 0;
-        if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
-        else v = read_row(data, p - row_offset);
-        sm.vals[i] = v;
+      // DELTA_BP / RLE data (no O(1) access, D-12): when the tile's positions span few
+      // data tiles, decode those once into a second buffer and pick the values there
+      __shared__ EngineSmem dsm;
+      __shared__ unsigned long long g_lo, g_hi;
+      const bool seq = data.format == MS_DELTA_BP || data.format == MS_RLE;
+      bool tiled = false;
+      if (seq) {
+        if (tid == 0) {
+          g_lo = ~0ull;
+          g_hi = 0;
+        }
+        __syncthreads();
+        unsigned long long lo = ~0ull, hi = 0;
+        for (uint32_t i = tid; i < cnt; i += kThreads) {
+          const uint64_t p = sm.vals[i];
+          lo = p < lo ? p : lo;
+          hi = p > hi ? p : hi;
+        }
+        atomicMin(&g_lo, lo);
+        atomicMax(&g_hi, hi);
+        __syncthreads();
+        const uint64_t plo = g_lo, phi = g_hi;
+        tiled = cnt && plo >= row_offset && phi - row_offset < data.n && (phi - plo) < 32ull * kChunk;
+        if (tiled) {
+          uint64_t v[kVPT];
+#pragma unroll
+          for (int q = 0; q < kVPT; ++q) v[q] = 0;
+          for (uint64_t dt = (plo - row_offset) / kChunk; dt <= (phi - row_offset) / kChunk; ++dt) {
+            const uint64_t d0 = dt * kChunk;
+            const uint32_t dcnt = (uint32_t)min((uint64_t)kChunk, data.n - d0);
+            load_rows(data, d0, dcnt, dsm);  // ends with a barrier
+#pragma unroll
+            for (int q = 0; q < kVPT; ++q) {
+              const uint32_t i = tid + q * kThreads;
+              if (i < cnt) {
+                const uint64_t r = sm.vals[i] - row_offset;
+                if (r >= d0 && r < d0 + dcnt) v[q] = dsm.vals[r - d0];
+              }
+            }
+            __syncthreads();
+          }
+#pragma unroll
+          for (int q = 0; q < kVPT; ++q) {
+            const uint32_t i = tid + q * kThreads;
+            if (i < cnt) sm.vals[i] = v[q];
+          }
+        }
+      }
+      if (!tiled) {
+        for (uint32_t i = tid; i < cnt; i += kThreads) {
+          const uint64_t p = sm.vals[i];
+          uint64_t v = 0;
+          if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
+          else v = read_row(data, p - row_offset);
+          sm.vals[i] = v;
+        }
       }
     }
     __syncthreads();

@@ -351,39 +351,7 @@ __device__ __forceinline__ void pack_lane_codes(uint32_t* buf, const uint64_t (&
   const uint32_t nw32 = PER * w;
   for (uint32_t i = lane; i < nw32; i += 32) buf[i] = 0;
   __syncwarp();
-  if (w) {
-    const uint32_t o = PER * lane * w;
-    uint32_t widx = o >> 5, nb = o & 31;
-    uint64_t acc = 0;
-    bool first = true;
-    auto flush = [&]() {
-      if (first) {
-        atomicOr(buf + widx, (uint32_t)acc);
-        first = false;
-      } else {
-        buf[widx] = (uint32_t)acc;
-      }
-      ++widx;
-      acc >>= 32;
-      nb -= 32;
-    };
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      if (w <= 32) {
-        acc |= c[q] << nb;
-        nb += w;
-        if (nb >= 32) flush();
-      } else {
-        acc |= (c[q] & 0xffffffffull) << nb;
-        nb += 32;
-        flush();
-        acc |= (c[q] >> 32) << nb;
-        nb += w - 32;
-        if (nb >= 32) flush();
-      }
-    }
-    if (nb) atomicOr(buf + widx, (uint32_t)acc);
-  }
+  stream_codes<PER>(buf, c, w, PER * lane * w);
   __syncwarp();
 }
 
