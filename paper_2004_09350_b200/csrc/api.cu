@@ -635,6 +635,7 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] 1 + max position
   const uint64_t o_bits = sc.add(4 * n_words, false);
   const uint64_t o_seg = sc.add(4 * (NS + 1), false);
+  const uint64_t o_list = sc.add(4 * ((NS * kSegRows + kChunk - 1) / kChunk + 2), false);  // pruning work list
   const uint64_t o_off = sc.add(8 * (NS + 1), false);  // the scan writes every entry
   const uint64_t o_gs = sc.add(8 * (items_max + 1), false);
   const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
@@ -653,7 +654,8 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   ColView src = view_of(in);
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
   uint64_t* seg_off = sc.at<uint64_t>(o_off);
-  MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, err, ctx.s));
+  MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, sc.at<uint32_t>(o_list),
+                            err, ctx.s));
   MS_TRY_CUDA(launch_seg_scan(sc.at<uint32_t>(o_seg), sc.at<uint32_t>(o_bits), NS, row_offset, G, seg_off,
                               sc.at<uint64_t>(o_gs), sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1),
                               sc.at<uint32_t>(o_tk1), ctx.s));

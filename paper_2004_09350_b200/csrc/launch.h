@@ -48,8 +48,9 @@ cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64
 cudaError_t launch_tile_copy(const OutView& o, uint64_t n_tiles, uint64_t nb, const uint64_t* cwx, uint32_t* err,
                              cudaStream_t s);
 // select core: bit mask (16 words per 512-row segment) + seg_info (count | last << 16)
+// tile_list: scratch of (NS * 512 / 2048 + 2) u32 for the header-only pruning of block formats (or nullptr)
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
-                          uint32_t* err, cudaStream_t s);
+                          uint32_t* tile_list, uint32_t* err, cudaStream_t s);
 // exclusive scan of per-segment counts -> seg_off[0..NS], start_seg[] per output item, 1 + max position
 // ... and, for every output item of G ranks starting in a segment, the item's first position
 cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint64_t NS, uint64_t row_offset,

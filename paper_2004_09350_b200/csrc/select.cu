@@ -81,14 +81,17 @@ __device__ __forceinline__ uint32_t tile_decision(const ColView& c, const Pred& 
 // are written (the fast kernel covers the others).
 template <class Pred>
 __global__ void __launch_bounds__(kThreads) select_generic_kernel(ColView c, Pred pred, uint32_t* bits,
-                                                                  uint32_t* seg_info, uint64_t s0, uint64_t s1) {
+                                                                  uint32_t* seg_info, uint64_t s0, uint64_t s1,
+                                                                  const uint32_t* list, const uint32_t* n_list) {
   __shared__ EngineSmem sm;
   __shared__ uint32_t words[kChunk / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t t0 = (s0 * kSegRows) / kChunk;
   const uint64_t t1 = (s1 * kSegRows + kChunk - 1) / kChunk;
   __shared__ uint32_t s_dec;
-  for (uint64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
+  const uint64_t n_iter = list ? *n_list : t1 - t0;  // the undecided tiles of tile_prune_kernel, or all
+  for (uint64_t it = blockIdx.x; it < n_iter; it += gridDim.x) {
+    const uint64_t t = list ? list[it] : t0 + it;
     const uint64_t r0 = t * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
     if (threadIdx.x == 0) s_dec = tile_decision(c, pred, r0, cnt);
@@ -142,6 +145,36 @@ cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cud
   return cudaGetLastError();
 }
 
+// Header-only pass over the tiles of a block-format column (one thread per tile):
+// a decided tile gets its 64 mask words and 4 segment counts written directly; the
+// others are listed for select_generic_kernel. At BJ.c3 (sorted values, a value
+// range covering ~2% of the column) all but a handful of tiles are decided here.
+__global__ void __launch_bounds__(256) tile_prune_kernel(ColView c, RangePred pred, uint32_t* bits,
+                                                         uint32_t* seg_info, uint64_t s0, uint64_t s1,
+                                                         uint32_t* list, uint32_t* n_list) {
+  const uint64_t t0 = (s0 * kSegRows) / kChunk;
+  const uint64_t t1 = (s1 * kSegRows + kChunk - 1) / kChunk;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = t0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += stride) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
+    const uint32_t dec = tile_decision(c, pred, r0, cnt);
+    if (dec == kDecode) {
+      list[atomicAdd(n_list, 1u)] = (uint32_t)t;
+      continue;
+    }
+    const uint32_t word = dec == kAll ? 0xffffffffu : 0u;
+    const uint32_t info = dec == kAll ? (uint32_t)kSegRows | ((uint32_t)kSegRows << 16) : 0u;
+    for (uint64_t sg = t * (kChunk / kSegRows); sg < (t + 1) * (kChunk / kSegRows); ++sg) {
+      if (sg < s0 || sg >= s1) continue;
+      uint4* wq = reinterpret_cast<uint4*>(bits + sg * kSegWords);
+#pragma unroll
+      for (int q = 0; q < kSegWords / 4; ++q) wq[q] = make_uint4(word, word, word, word);
+      seg_info[sg] = info;
+    }
+  }
+}
+
 // RLE: the predicate is evaluated once per run (P:163's per-run view of
 // the column); a matching run sets its row range in the mask — whole 32-bit words
 // by plain stores, the (at most two) partial words by atomicOr — and the
@@ -185,7 +218,7 @@ __global__ void __launch_bounds__(256) seg_info_kernel(const uint32_t* bits, uin
 }
 
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
-                          uint32_t* err, cudaStream_t s) {
+                          uint32_t* tile_list, uint32_t* err, cudaStream_t s) {
   if (NS == 0) return cudaSuccess;
   if (c.format == MS_RLE && c.run_starts) {
     cudaError_t e = cudaMemsetAsync(bits, 0, 4 * NS * kSegWords, s);
@@ -251,15 +284,28 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
   }
   if (ns_fast < NS) {  // the rest (other formats, partial segments, block remainders)
     const uint64_t tiles = ((NS * kSegRows + kChunk - 1) / kChunk) - (ns_fast * kSegRows) / kChunk;
+    const bool prune = !p.is_bitmap && tile_list &&
+                       (c.format == MS_DELTA_BP || c.format == MS_FOR_BP || c.format == MS_DYN_BP);
+    uint32_t* n_list = prune ? tile_list + tiles + 1 : nullptr;
+    if (prune) {  // header-only decisions first; only undecided tiles are decoded
+      cudaError_t e = cudaMemsetAsync(n_list, 0, 4, s);
+      if (e != cudaSuccess) return e;
+      uint64_t g = (tiles + 255) / 256;
+      if (g > (uint64_t)num_sms() * 8) g = num_sms() * 8;
+      ProfScope prof_("select_prune", s);
+      tile_prune_kernel<<<(int)g, 256, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits, seg_info, ns_fast, NS,
+                                                tile_list, n_list);
+    }
     ProfScope prof_("select_generic", s);
     if (p.is_bitmap) {
       auto k = select_generic_kernel<BitmapPred>;
       k<<<persistent_grid(k, kThreads, tiles), kThreads, 0, s>>>(c, BitmapPred{p.bitmap, p.bitmap_bits}, bits,
-                                                                 seg_info, ns_fast, NS);
+                                                                 seg_info, ns_fast, NS, nullptr, nullptr);
     } else {
       auto k = select_generic_kernel<RangePred>;
       k<<<persistent_grid(k, kThreads, tiles), kThreads, 0, s>>>(c, RangePred{p.lo, p.span, p.neg}, bits,
-                                                                 seg_info, ns_fast, NS);
+                                                                 seg_info, ns_fast, NS,
+                                                                 prune ? tile_list : nullptr, n_list);
     }
   }
   return cudaGetLastError();
