@@ -306,16 +306,42 @@ struct EngineSmem {
 __device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_t cnt, EngineSmem& sm) {
   const int tid = threadIdx.x;
   switch (c.format) {
-    case MS_UNCOMPR:
-      for (uint32_t i = tid; i < cnt; i += kThreads) sm.vals[i] = __ldg(c.payload + r0 + i);
+    // the O(1) formats: all kVPT loads of a thread issued before any is stored
+    // (a runtime-bounded loop would serialise one memory latency per row)
+    case MS_UNCOMPR: {
+      uint64_t v[kVPT];
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const uint32_t i = tid + q * kThreads;
+        v[q] = i < cnt ? __ldg(c.payload + r0 + i) : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) sm.vals[tid + q * kThreads] = v[q];
       break;
-    case MS_STATIC_BP:
-      for (uint32_t i = tid; i < cnt; i += kThreads) sm.vals[i] = unpack_at(c.payload, (r0 + i) * c.w, c.w);
+    }
+    case MS_STATIC_BP: {
+      uint64_t v[kVPT];
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const uint32_t i = tid + q * kThreads;
+        v[q] = i < cnt ? unpack_at(c.payload, (r0 + i) * c.w, c.w) : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) sm.vals[tid + q * kThreads] = v[q];
       break;
+    }
     case MS_DYN_BP:
-    case MS_FOR_BP:
-      for (uint32_t i = tid; i < cnt; i += kThreads) sm.vals[i] = read_row(c, r0 + i);
+    case MS_FOR_BP: {
+      uint64_t v[kVPT];
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const uint32_t i = tid + q * kThreads;
+        v[q] = i < cnt ? read_row(c, r0 + i) : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) sm.vals[tid + q * kThreads] = v[q];
       break;
+    }
     case MS_DELTA_BP: {
       // thread t owns rows [8t, 8t+8): local prefix of the deltas, CTA scan,
       // then subtract the prefix at the block head (segmented scan).

@@ -35,15 +35,16 @@ struct OutView {
 };
 
 // Output word m (bits [64m, 64m+64)) of a packed stream of `cnt` codes of width
-// w (1..64); code(j) yields the j-th code, already < 2^w.
+// w (1..64), m < 2^14 (a tile: <= 2048 codes); code(j) yields the j-th code,
+// already < 2^w. 32-bit index math with a multiply-high division (div_small).
 template <class CodeFn>
-__device__ __forceinline__ uint64_t pack_word(CodeFn code, uint32_t cnt, uint32_t w, uint64_t m) {
-  const uint64_t bit0 = m * 64;
-  uint32_t j = (uint32_t)(bit0 / w);
-  const uint32_t s = (uint32_t)(bit0 - (uint64_t)j * w);
+__device__ __forceinline__ uint64_t pack_word(CodeFn code, uint32_t cnt, uint32_t w, uint32_t m, uint32_t magic) {
+  const uint32_t bit0 = m * 64;
+  uint32_t j = div_small(bit0, w, magic);
+  const uint32_t s = bit0 - j * w;
   uint64_t acc = j < cnt ? code(j) >> s : 0;
   for (++j; j < cnt; ++j) {
-    const uint64_t jb = (uint64_t)j * w;
+    const uint32_t jb = j * w;
     if (jb >= bit0 + 64) break;
     acc |= code(j) << (jb - bit0);
   }
@@ -81,7 +82,8 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
       const uint64_t wbase = (uint64_t)item * (kChunk / 64) * w;
       const uint64_t nwords = ((uint64_t)cnt * w + 63) / 64;
       auto code = [&](uint32_t j) { return sm.vals[j] & mask; };
-      for (uint64_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, cnt, w, m);
+      const uint32_t magic = 0xffffffffu / w + 1u;
+      for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, cnt, w, m, magic);
       return;
     }
     default:
@@ -110,8 +112,19 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
         lmin = c < lmin ? c : lmin;
         lmax = c > lmax ? c : lmax;
       }
-      if (o.format == MS_FOR_BP) atomicMin((unsigned long long*)&sm.bmin[blk], (unsigned long long)lmin);
-      atomicMax((unsigned long long*)&sm.bmax[blk], (unsigned long long)lmax);
+      // reduce over the B/8 threads of the block inside the warp first (B >= 128:
+      // groups of >= 16 lanes), then one shared atomic per group
+      const uint32_t grp = (B / kVPT) < 32u ? (B / kVPT) : 32u;
+      const unsigned gm = grp == 32 ? kFull : (((1u << grp) - 1) << ((tid & 31) & ~(grp - 1)));
+      for (uint32_t sh = grp >> 1; sh > 0; sh >>= 1) {
+        const uint64_t a = __shfl_xor_sync(gm, lmin, sh), b = __shfl_xor_sync(gm, lmax, sh);
+        lmin = a < lmin ? a : lmin;
+        lmax = b > lmax ? b : lmax;
+      }
+      if (((tid & 31) & (grp - 1)) == 0) {
+        if (o.format == MS_FOR_BP) atomicMin((unsigned long long*)&sm.bmin[blk], (unsigned long long)lmin);
+        atomicMax((unsigned long long*)&sm.bmax[blk], (unsigned long long)lmax);
+      }
     }
   }
   __syncthreads();
@@ -147,16 +160,17 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     uint64_t* const dst = o.slots ? o.slots + (uint64_t)item * kChunk : o.payload;  // tile slot or final place
     const uint64_t wbase = sm.bex[bi] * (B / 64);
     const uint32_t nwords = (B / 64) * w;
+    const uint32_t magic = 0xffffffffu / w + 1u;
     if (o.format == MS_FOR_BP) {
       const uint64_t rf = sm.bmin[bi];
       auto code = [&](uint32_t j) { return v[j] - rf; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m);
+      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
     } else if (o.format == MS_DELTA_BP) {
       auto code = [&](uint32_t j) { return j ? v[j] - v[j - 1] : 0ull; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m);
+      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
     } else {
       auto code = [&](uint32_t j) { return v[j]; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m);
+      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
     }
   }
   const uint32_t rem_cnt = cnt - (nbc << lg);

@@ -1,0 +1,12 @@
+python - <<'PY'
+import sys; sys.path.insert(0,'.')
+import torch, synth
+from paper_2004_09350_b200 import ms
+n = 1 << 27
+x = synth.gen_torch("c3.x", n)
+D = ms.compress(x, ms.delta_bp(2048))
+torch.cuda.synchronize()
+D = ms.compress(x, ms.delta_bp(2048))
+torch.cuda.synchronize()
+print("ok", D.n)
+PY
