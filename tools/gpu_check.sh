@@ -16,9 +16,12 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$N
   -o /tmp/${TAG}_prof python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu $BENCH_ARGS > $O/${TAG}_ncu_full.log 2>&1
 ncu -i /tmp/${TAG}_prof.ncu-rep --page raw --csv > $O/${TAG}_raw.csv 2>&1
 ncu -i /tmp/${TAG}_prof.ncu-rep --page details --csv > $O/${TAG}_details.csv 2>&1
-ncu -i /tmp/${TAG}_prof.ncu-rep --page source --csv --print-source cuda,sass > $O/${TAG}_source.csv 2>&1
+if [ -n "$NCU_SOURCE" ]; then
+ncu -i /tmp/${TAG}_prof.ncu-rep --page source --csv --print-source cuda,sass > /tmp/${TAG}_source.csv 2>&1
+python tools/ncu_lines.py /tmp/${TAG}_source.csv "" 60 > $O/${TAG}_lines.txt 2>&1
+fi
 sz=$(stat -c %s /tmp/${TAG}_prof.ncu-rep)
-if [ "$sz" -lt 40000000 ]; then cp /tmp/${TAG}_prof.ncu-rep $O/; fi
+if [ "$sz" -lt 20000000 ]; then cp /tmp/${TAG}_prof.ncu-rep $O/; fi
 fi
 du -sh $O
 echo done
