@@ -72,6 +72,11 @@ def c2(reps):
     n = 1 << 28
     X = ms.compress(synth.gen_torch("c2.X", n), ms.dyn_bp(512))
     Y = ms.compress(synth.gen_torch("c2.Y", n), ms.for_bp(512))
+    xu = synth.gen_torch("c2.X", n)
+    report("c2", "compress u64 -> DYN_BP{512}", timed(lambda: ms.compress(xu, ms.dyn_bp(512)), reps), n,
+           8 * n + X.footprint())
+    del xu
+    report("c2", "sum X (whole column)", timed(lambda: ms.agg_sum(X), reps), n, X.footprint())
     pos = ms.select(X, ms.EQ, 17, out_fmt=ms.delta_bp(512))
     report("c2", "select X==17 -> DELTA_BP{512}", timed(lambda: ms.select(X, ms.EQ, 17, out_fmt=ms.delta_bp(512)),
                                                         reps), n, X.footprint() + pos.footprint())
@@ -94,6 +99,14 @@ def c3(reps):
                C.footprint() + pos.footprint())
         report("c3", f"sum {name} at positions", timed(lambda: ms.agg_sum(C, pos), reps), pos.n,
                pos.footprint() + C.footprint())
+    report("c3", "decompress DELTA_BP{2048} -> u64", timed(lambda: ms.decompress(D), reps), n,
+           D.footprint() + 8 * n)
+    report("c3", "decompress RLE -> u64", timed(lambda: ms.decompress(R), reps), n, R.footprint() + 8 * n)
+    xr = ms.decompress(D)
+    report("c3", "compress u64 -> DELTA_BP{2048}", timed(lambda: ms.compress(xr, ms.delta_bp(2048)), reps), n,
+           8 * n + D.footprint())
+    report("c3", "compress u64 -> RLE", timed(lambda: ms.compress(xr, ms.rle()), reps), n, 8 * n + R.footprint())
+    del xr
     m1 = ms.morph(R, ms.delta_bp(2048))
     report("c3", "morph RLE -> DELTA_BP{2048}", timed(lambda: ms.morph(R, ms.delta_bp(2048)), reps), n,
            R.footprint() + m1.footprint())
