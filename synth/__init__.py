@@ -88,6 +88,9 @@ RECIPES = {
                            skew=(seed(20), 1 << 62, 10)),
     "C3.Y": lambda: recipe(SYN_MASK, seed=seed(22), mask=63, add=1 << 62),
     "C4.Y": lambda: recipe(SYN_RANGE, seed=seed(22), m=100_001, add=1 << 47, sorted_=True),
+    # C4 with the select benchmark's 90% lowest-value skew, then sorted
+    "C4.X": lambda: recipe(SYN_RANGE, seed=seed(22), m=100_001, add=1 << 47, sorted_=True,
+                           skew=(seed(20), 1 << 47, 10)),
 }
 
 _host = None
