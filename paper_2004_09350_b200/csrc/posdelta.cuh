@@ -164,42 +164,9 @@ __device__ __forceinline__ uint64_t pd_walk(const uint32_t* __restrict__ bits, u
 // the contiguous bit range [PER*j*w, PER*(j+1)*w) — into buf (B*w/32 u32,
 // zeroed here): plain stores inside the range, atomicOr on the two words it
 // may share with its neighbours; returns w.
-template <int PER, bool PACK, bool AUTO_W = false>
-__device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
-                                                 uint64_t span_words, uint32_t w, uint32_t* stage, uint32_t* buf,
-                                                 uint32_t lane) {
-  const uint64_t wi = row0 >> 5;
-  const uint32_t fmask = ~0u << (row0 & 31);
-  const uint64_t wa = wi & ~3ull;
-  const uint32_t need = (uint32_t)((wi - wa) + span_words);
-  const uint32_t C = ((need + 127) / 128) * 4;  // words per lane, multiple of 4, 32*C >= need
-  const uint32_t wi_rel = (uint32_t)(wi - wa);
-  // 1. stage + count
-  const uint64_t c0 = wa + (uint64_t)C * lane;
-  uint4* st4 = reinterpret_cast<uint4*>(stage) + (C / 4) * lane;
-  uint32_t cnt = 0;
-  for (uint32_t q = 0; q < C; q += 4) {
-    const uint64_t m = c0 + q;
-    uint32_t x0, x1, x2, x3;
-    if (m + 4 <= n_words) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4*>(bits + m));
-      x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w;
-    } else {
-      x0 = m < n_words ? __ldg(bits + m) : 0u;
-      x1 = m + 1 < n_words ? __ldg(bits + m + 1) : 0u;
-      x2 = m + 2 < n_words ? __ldg(bits + m + 2) : 0u;
-      x3 = 0u;
-    }
-    if (m == wa) {  // the first four words hold the block start (wi - wa < 4)
-      x0 = wi_rel > 0 ? 0u : x0 & fmask;
-      x1 = wi_rel > 1 ? 0u : (wi_rel == 1 ? x1 & fmask : x1);
-      x2 = wi_rel > 2 ? 0u : (wi_rel == 2 ? x2 & fmask : x2);
-      x3 = wi_rel == 3 ? x3 & fmask : x3;
-    }
-    st4[q / 4] = make_uint4(x0, x1, x2, x3);
-    cnt += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
-  }
-  __syncwarp();
+template <int PER, bool PACK, bool AUTO_W>
+__device__ __forceinline__ uint32_t pd_after_stage(uint32_t cnt, uint32_t C, uint64_t wa, uint32_t w,
+                                                   const uint32_t* stage, uint32_t* buf, uint32_t lane) {
   uint32_t inc = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -275,6 +242,45 @@ __device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bi
   }
   __syncwarp();
   return w;
+}
+
+template <int PER, bool PACK, bool AUTO_W = false>
+__device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
+                                                 uint64_t span_words, uint32_t w, uint32_t* stage, uint32_t* buf,
+                                                 uint32_t lane) {
+  const uint64_t wi = row0 >> 5;
+  const uint32_t fmask = ~0u << (row0 & 31);
+  const uint64_t wa = wi & ~3ull;
+  const uint32_t need = (uint32_t)((wi - wa) + span_words);
+  const uint32_t C = ((need + 127) / 128) * 4;  // words per lane, multiple of 4, 32*C >= need
+  const uint32_t wi_rel = (uint32_t)(wi - wa);
+  // 1. stage + count
+  const uint64_t c0 = wa + (uint64_t)C * lane;
+  uint4* st4 = reinterpret_cast<uint4*>(stage) + (C / 4) * lane;
+  uint32_t cnt = 0;
+  for (uint32_t q = 0; q < C; q += 4) {
+    const uint64_t m = c0 + q;
+    uint32_t x0, x1, x2, x3;
+    if (m + 4 <= n_words) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(bits + m));
+      x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w;
+    } else {
+      x0 = m < n_words ? __ldg(bits + m) : 0u;
+      x1 = m + 1 < n_words ? __ldg(bits + m + 1) : 0u;
+      x2 = m + 2 < n_words ? __ldg(bits + m + 2) : 0u;
+      x3 = 0u;
+    }
+    if (m == wa) {  // the first four words hold the block start (wi - wa < 4)
+      x0 = wi_rel > 0 ? 0u : x0 & fmask;
+      x1 = wi_rel > 1 ? 0u : (wi_rel == 1 ? x1 & fmask : x1);
+      x2 = wi_rel > 2 ? 0u : (wi_rel == 2 ? x2 & fmask : x2);
+      x3 = wi_rel == 3 ? x3 & fmask : x3;
+    }
+    st4[q / 4] = make_uint4(x0, x1, x2, x3);
+    cnt += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
+  }
+  __syncwarp();
+  return pd_after_stage<PER, PACK, AUTO_W>(cnt, C, wa, w, stage, buf, lane);
 }
 
 __device__ __forceinline__ bool pd_span(const uint64_t* gstart, uint64_t item, uint64_t n_items, uint64_t row0,

@@ -76,6 +76,16 @@ def c2():
     prof("select c2", lambda: ms.select(X, ms.EQ, 17, out_fmt=ms.delta_bp(512)))
 
 
+def sweep():
+    import numpy as np
+    n = 1 << 27
+    v = synth.gen_host("C1.X", n)
+    t = torch.from_numpy(v.view(np.int64)).cuda()
+    X = ms.compress(t, ms.static_bp(0))
+    for f, name in ((ms.uncompr(), "UNCOMPR"), (ms.delta_bp(512), "DELTA_BP512"), (ms.dyn_bp(512), "DYN_BP512")):
+        prof(f"C1 static -> {name}", lambda: ms.select(X, ms.EQ, 0, out_fmt=f))
+
+
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     for c in (sys.argv[1:] or ["c2", "c3", "c4"]):
