@@ -641,12 +641,16 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
   const uint64_t o_tk1 = sc.add(8, true);
   const bool pos_delta = out_fmt.format == MS_DELTA_BP && G <= 512;  // posdelta.cuh
-  const uint64_t o_st2 = sc.add(pos_delta ? 8 : 8 * (items_max + 1), true);  // look-back status (other formats)
+  // other formats with items <= 512: the slot encoder (MaskSource), no look-back
+  const bool pos_slots = !pos_delta && G <= 512 && out_fmt.format != MS_RLE && !env_flag("MS_ENCODE_TICKET") &&
+                         !env_flag("MS_POS_DEFERRED");
+  const uint64_t o_st2 = sc.add(pos_delta || pos_slots ? 8 : 8 * (items_max + 1), true);  // look-back status
   const uint64_t o_tk2 = sc.add(8, true);
-  const uint64_t o_wk = pos_delta ? sc.add(4 * (items_max + 1), false) : 0;
-  const uint64_t o_cwx = pos_delta ? sc.add(8 * (items_max + 2), false) : 0;
-  const uint64_t o_st3 = pos_delta ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
-  const uint64_t o_tk3 = pos_delta ? sc.add(8, true) : 0;
+  const bool wscan = pos_delta || pos_slots;
+  const uint64_t o_wk = wscan ? sc.add(4 * (items_max + 1), false) : 0;
+  const uint64_t o_cwx = wscan ? sc.add(8 * (items_max + 2), false) : 0;
+  const uint64_t o_st3 = wscan ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
+  const uint64_t o_tk3 = wscan ? sc.add(8, true) : 0;
   RlePrep rp;
   plan_rle(sc, in, rp);
   if (!sc.commit()) return MS_E_NOMEM;
@@ -721,11 +725,20 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
       slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
       if (!slots) { release(ctx, out); return MS_E_NOMEM; }
     }
+    if (pos_slots && is_block(f.format) && n_out / G) {  // DYN_BP / FOR_BP positions: 64-bit slots
+      slot_words = G;  // G / 64 * 64
+      slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
+      if (!slots) { release(ctx, out); return MS_E_NOMEM; }
+    }
     cudaError_t e =
         pos_delta && f.format == MS_DELTA_BP
             ? launch_positions_delta(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
                                      sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
                                      sc.at<uint32_t>(o_tk3), slots, slot_words, err, ctx.s)
+        : pos_slots
+            ? launch_positions_slots(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset, slots,
+                                     slot_words, sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx),
+                                     sc.at<uint64_t>(o_st3), sc.at<uint32_t>(o_tk3), err, ctx.s)
             : launch_positions(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
                                sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
     ctx.free(slots);  // stream-ordered free: the copy kernel is queued before it

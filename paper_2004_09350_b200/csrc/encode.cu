@@ -189,6 +189,45 @@ cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_
   return run_warp_encode(ProjectSource<4>{pos, data, row_offset, pf}, e, status, ticket, err, "project_warp", s);
 }
 
+// select positions in a format other than DELTA_BP (items <= 512): MaskSource into
+// the slot encoder; block formats then scan the widths and copy (no look-back)
+cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                                   uint64_t row_offset, uint64_t* slots, uint32_t slot_words, uint32_t* wk,
+                                   uint64_t* cwx, uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err,
+                                   cudaStream_t s) {
+  const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
+  const uint64_t n_full = e.n_out / e.G;
+  if (!n_items) return cudaSuccess;
+  const MaskSource src{bits, NS, gstart, row_offset};
+  auto launch = [&](auto k) {
+    const int warps = 4;
+    const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)per_sm * num_sms();
+    const uint64_t need = (n_items + warps - 1) / warps;
+    if (need < grid) grid = need;
+    ProfScope prof_("pos_encode", s);
+    k<<<(int)grid, warps * 32, smem, s>>>(src, e, n_items, slots, slot_words, wk, err);
+    return cudaGetLastError();
+  };
+  cudaError_t r = e.G == 512   ? launch(warp_encode_slot_kernel<MaskSource, 16>)
+                  : e.G == 256 ? launch(warp_encode_slot_kernel<MaskSource, 8>)
+                               : launch(warp_encode_slot_kernel<MaskSource, 4>);
+  if (r != cudaSuccess) return r;
+  const bool block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  if (!block || !n_full) return cudaSuccess;
+  r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
+  if (r != cudaSuccess) return r;
+  uint64_t cgrid = (n_full + 7) / 8;
+  if (cgrid > (uint64_t)num_sms() * 8) cgrid = num_sms() * 8;
+  ProfScope prof_("pos_copy", s);
+  pos_copy_kernel<<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
+  return cudaGetLastError();
+}
+
 // project with per-block slots (no look-back): gather + encode into slots, scan the
 // widths, copy the blocks to their places (pos_copy_kernel is format-agnostic).
 cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e0,

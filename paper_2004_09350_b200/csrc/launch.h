@@ -78,6 +78,11 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
                                    uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
                                    uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* err,
                                    cudaStream_t s);
+// select positions in other formats (items <= 512) through the slot encoder (+ scan, copy for block formats)
+cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
+                                   uint64_t row_offset, uint64_t* slots, uint32_t slot_words, uint32_t* wk,
+                                   uint64_t* cwx, uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err,
+                                   cudaStream_t s);
 // project through the warp encoder (positions DELTA_BP with B == G, or O(1) formats; data O(1) formats)
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);

@@ -53,3 +53,26 @@ def test_positions_clustered(walk):
         g = ms.select(X, ms.EQ, 1, out_fmt=ms.delta_bp(B))
         o = O.select(oX, O.EQ, 1, out_fmt=O.DELTA_BP, out_block=B)
         assert_same_image(g, o, f"clustered B={B}")
+
+
+@pytest.mark.parametrize("deferred", [False, True])
+@pytest.mark.parametrize("sel", [0.9, 0.0625, 0.003])
+def test_positions_other_formats(sel, deferred, monkeypatch):
+    """Positions as UNCOMPR / STATIC_BP / DYN_BP / FOR_BP (slot encoder, or the
+    deferred look-back encoder with MS_POS_DEFERRED=1), byte-exact."""
+    if deferred:
+        monkeypatch.setenv("MS_POS_DEFERRED", "1")
+    ms = get_ms()
+    rng = np.random.default_rng(int(sel * 1000) + 3)
+    n = 400_003
+    v = rng.integers(0, 1 << 20, n).astype(np.uint64)
+    thr = int(sel * (1 << 20))
+    X = ms.compress(to_torch(v), ms.dyn_bp(512))
+    oX = O.encode(v, O.DYN_BP, 0, 512)
+    for fo, of in ((ms.uncompr(), (O.UNCOMPR, 0, 0)), (ms.static_bp(0), (O.STATIC_BP, 0, 0)),
+                   (ms.static_bp(40), (O.STATIC_BP, 40, 0)), (ms.dyn_bp(512), (O.DYN_BP, 0, 512)),
+                   (ms.for_bp(256), (O.FOR_BP, 0, 256)), (ms.dyn_bp(128), (O.DYN_BP, 0, 128))):
+        for off in (0, 1 << 33):
+            g = ms.select(X, ms.LT, thr, row_offset=off, out_fmt=fo)
+            o = O.select(oX, O.LT, thr, row_offset=off, out_fmt=of[0], out_width=of[1], out_block=of[2] or 512)
+            assert_same_image(g, o, f"sel={sel} -> {fo} off={off} deferred={deferred}")
