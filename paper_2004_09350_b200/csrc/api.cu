@@ -294,11 +294,15 @@ ms_status readback(const Ctx& ctx, const uint64_t* dev, uint64_t* host, size_t c
 
 // finish an output: read the error word and, for block formats, cw[nb] and
 // the largest block width (the max_width hint of the descriptor)
-ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev) {
+ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev,
+                        const uint64_t* maxw_pre = nullptr) {
   uint64_t h[2] = {0, 0};
   uint32_t maxw = 0;
+  uint64_t maxw64 = 0;
   uint32_t* maxw_dev = nullptr;
-  if (is_block(out->fmt.format) && out->n_blocks) {
+  if (is_block(out->fmt.format) && out->n_blocks && maxw_pre) {  // the width scan's maximum
+    MS_TRY_CUDA(cudaMemcpyAsync(&maxw64, maxw_pre, 8, cudaMemcpyDeviceToHost, ctx.s));
+  } else if (is_block(out->fmt.format) && out->n_blocks) {
     maxw_dev = (uint32_t*)ctx.alloc(4);
     if (!maxw_dev) return MS_E_NOMEM;
     cudaError_t e = cudaMemsetAsync(maxw_dev, 0, 4, ctx.s);
@@ -315,6 +319,7 @@ ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev)
   MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
   ctx.free(maxw_dev);
   MS_TRY_CUDA(cudaGetLastError());
+  if (maxw_pre) maxw = (uint32_t)maxw64;
   const ms_status st = status_from_bits((uint32_t)h[0]);
   if (st != MS_OK) return st;
   if (is_block(out->fmt.format)) {
@@ -431,12 +436,13 @@ ms_status encode_into(const Ctx& ctx, Scratch& sc, uint64_t meta_off, uint64_t s
   cudaError_t e = launch(ov);
   if (e == cudaSuccess && slot_mode) e = launch_count_scan(ov.bw, nb, cwx, scan_st, scan_tk, ctx.s);
   if (e == cudaSuccess && slot_mode) e = launch_tile_copy(ov, n_tiles, nb, cwx, err, ctx.s);
-  ctx.free(slot_mem);  // stream-ordered
   if (e != cudaSuccess) {
+    ctx.free(slot_mem);
     release(ctx, out);
     return cuda_status(e);
   }
-  ms_status st = finish_output(ctx, out, err);
+  ms_status st = finish_output(ctx, out, err, slot_mode ? cwx + nb + 1 : nullptr);
+  ctx.free(slot_mem);
   if (st == MS_OK) st = maybe_shrink(ctx, out);
   if (st != MS_OK) release(ctx, out);
   return st;
@@ -449,7 +455,7 @@ ms_status compress_rle(const Ctx& ctx, const uint64_t* values, uint64_t n, ms_co
   Scratch sc(ctx);
   const uint64_t o_meta = sc.add(64, true);
   const uint64_t o_cnt = sc.add(4 * (T + 1), false);
-  const uint64_t o_off = sc.add(8 * (T + 1), true);
+  const uint64_t o_off = sc.add(8 * (T + 2), true);
   const uint64_t o_st = sc.add(8 * ((T + kChunk - 1) / kChunk + 1), true);
   const uint64_t o_tk = sc.add(8, true);
   if (!sc.commit()) return MS_E_NOMEM;
@@ -747,7 +753,8 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
       return cuda_status(e);
     }
   }
-  ms_status st = finish_output(ctx, out, err);
+  const bool wmax_known = (pos_delta || pos_slots) && is_block(f.format) && n_out / G;
+  ms_status st = finish_output(ctx, out, err, wmax_known ? sc.at<uint64_t>(o_cwx) + n_out / G + 1 : nullptr);
   if (st == MS_OK) st = maybe_shrink(ctx, out);
   if (st != MS_OK) release(ctx, out);
   return st;
@@ -847,7 +854,8 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
       release(ctx, out);
       return cuda_status(e);
     }
-    ms_status st = finish_output(ctx, out, err);
+    ms_status st = finish_output(ctx, out, err,
+                                 slotted && is_block(f.format) && n / G ? sc.at<uint64_t>(o_cwx) + n / G + 1 : nullptr);
     if (st == MS_OK) st = maybe_shrink(ctx, out);
     if (st != MS_OK) release(ctx, out);
     return st;

@@ -349,16 +349,23 @@ cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint
                   ticket, s);
 }
 
-struct CountEpi : NoKey {
+// exclusive prefix into off[0..T), total into off[T], the largest count into off[T + 1]
+// (block widths: the output's max_width hint without a separate pass)
+struct CountEpi {
   uint64_t* off;
   uint64_t T;
+  const uint32_t* cnt;
   __device__ void operator()(uint64_t idx, uint64_t o, uint64_t c) const { off[idx] = o; }
   __device__ void total(uint64_t t) const { off[T] = t; }
+  __device__ uint64_t key(uint64_t idx) const { return cnt[idx]; }
+  __device__ void max_key(uint64_t k) const { atomicMax(reinterpret_cast<unsigned long long*>(off + T + 1), k); }
 };
 
 cudaError_t launch_count_scan(const uint32_t* counts, uint64_t T, uint64_t* off, uint64_t* status,
                               uint32_t* ticket, cudaStream_t s) {
-  return run_scan(U32In{counts}, CountEpi{{}, off, T}, T, status, ticket, s);
+  cudaError_t e = cudaMemsetAsync(off + T + 1, 0, 8, s);
+  if (e != cudaSuccess) return e;
+  return run_scan(U32In{counts}, CountEpi{off, T, counts}, T, status, ticket, s);
 }
 
 // RLE: run starts = exclusive prefix of the lengths; lengths must be >= 1 and

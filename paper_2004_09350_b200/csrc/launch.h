@@ -99,6 +99,7 @@ cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, u
 cudaError_t launch_chunk_run(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run, cudaStream_t s);
 // RLE compression of raw device values
 cudaError_t launch_rle_count(const uint64_t* v, uint64_t n, uint32_t* counts, cudaStream_t s);
+// off: T + 2 entries (exclusive prefix, total, max count)
 cudaError_t launch_count_scan(const uint32_t* counts, uint64_t T, uint64_t* off, uint64_t* status,
                               uint32_t* ticket, cudaStream_t s);
 cudaError_t launch_rle_write(const uint64_t* v, uint64_t n, const uint64_t* chunk_off, uint64_t* payload,
