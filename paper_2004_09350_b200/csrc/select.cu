@@ -263,17 +263,16 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
       ProfScope prof_("select_fast", s);
       k<<<grid, warps_per_cta * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, spw, err, nullptr);
     };
-    // variants (stages, warps/CTA, min CTAs/SM); default measured on B200, env override for experiments
-    const int v = env_int("MS_SELECT_VARIANT", 0);
-    // narrow staging slots (2 x 2 KiB per pair) when every block is <= 32 bits wide
+    // staging slots sized from the descriptor's max_width hint: narrow (<= 32 bits, 2 x 2 KiB
+    // per pair, 6 CTAs/SM), medium (<= 48 bits, 4 CTAs/SM) or wide (3 CTAs/SM). Measured on B200
+    // (BJ.c5): 3-stage and 8-warp variants of the narrow kernel were 8-50% slower.
     const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
-#define MS_PICK(K)                                                             \
-  do {                                                                         \
-    if (v == 1) pick(select_fast_kernel<K, 3, 4, 2>, 3, 4);                    \
-    else if (v == 2) pick(select_fast_kernel<K, 2, 8, 1>, 2, 8);               \
-    else if (v == 3) pick(select_fast_kernel<K, 3, 4, 4, kPairBufNarrow>, 3, 4, kPairBufNarrow); \
-    else if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow); \
-    else pick(select_fast_kernel<K, 2, 4, 3>, 2, 4);                           \
+    const bool medium = !narrow && c.maxw >= 33 && c.maxw <= 48 && !env_int("MS_SELECT_NO_MEDIUM", 0);
+#define MS_PICK(K)                                                                                   \
+  do {                                                                                               \
+    if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow);          \
+    else if (medium) pick(select_fast_kernel<K, 2, 4, 4, kPairBufMedium>, 2, 4, kPairBufMedium);     \
+    else pick(select_fast_kernel<K, 2, 4, 3>, 2, 4);                                                 \
   } while (0)
     if (kind == FAST_UNCOMPR) MS_PICK(FAST_UNCOMPR);
     else if (kind == FAST_STATIC) MS_PICK(FAST_STATIC);

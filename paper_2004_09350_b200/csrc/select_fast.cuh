@@ -259,6 +259,7 @@ enum : int { CORE_SELECT = 0, CORE_SUM = 1 };
 // widths / references travel with the slot.
 constexpr int kPairBufWide = 2048 + 16;   // two segments at up to 64 bits + padding
 constexpr int kPairBufNarrow = 1024 + 16; // two segments at up to 32 bits + padding
+constexpr int kPairBufMedium = 1536 + 16; // two segments at up to 48 bits + padding
 template <int KIND, int kStages = 2, int kFastWarps = 4, int kMinBlocks = 3, int kPairBufU32 = kPairBufWide,
           int CORE = CORE_SELECT>
 __global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kernel(ColView c, FastPred pred,
