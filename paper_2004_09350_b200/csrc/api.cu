@@ -598,6 +598,54 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
     }
     return MS_OK;
   }
+  if (in->fmt.format == MS_RLE && fmt.format == MS_DELTA_BP && !env_flag("MS_MORPH_ENGINE")) {
+    // direct morph: from the runs alone (morph.cu)
+    const uint32_t B = fmt.block_size;
+    const uint64_t nb = n / B, nrem = n % B;
+    Scratch sc(ctx);
+    const uint64_t o_meta = sc.add(64, true);
+    const uint64_t o_wk = sc.add(4 * (nb + 1), false);
+    const uint64_t o_cwx = sc.add(8 * (nb + 2), false);
+    const uint64_t o_ref = sc.add(8 * (nb + 1), false);
+    const uint64_t o_rem = sc.add(8 * (nrem + 1), false);
+    const uint64_t o_st = sc.add(8 * ((nb + kChunk - 1) / kChunk + 1), true);
+    const uint64_t o_tk = sc.add(8, true);
+    RlePrep rp;
+    plan_rle(sc, in, rp);
+    if (!sc.commit()) return MS_E_NOMEM;
+    uint32_t* err = sc.at<uint32_t>(o_meta);
+    ColView src = view_of(in);
+    MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+    MS_TRY_CUDA(launch_rle2delta_widths(src, B, nb, sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_ref),
+                                        sc.at<uint64_t>(o_rem), ctx.s));
+    uint64_t h[2] = {0, 0};
+    if (nb) {
+      MS_TRY_CUDA(launch_count_scan(sc.at<uint32_t>(o_wk), nb, sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st),
+                                    sc.at<uint32_t>(o_tk), ctx.s));
+      MS_TRY_CUDA(cudaMemcpyAsync(&h[1], sc.at<uint64_t>(o_cwx) + nb, 8, cudaMemcpyDeviceToHost, ctx.s));
+    }
+    MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 1));
+    MS_TRY(status_from_bits((uint32_t)h[0]));
+    if (h[1] > 0xffffffffull) return MS_E_INVALID;  // D-4 limit
+    const uint64_t words = h[1] * (B / 64);
+    MS_TRY(alloc_column(ctx, out, fmt, n, words, 0));
+    out->payload_words = words;
+    cudaError_t e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
+    if (e == cudaSuccess && words) e = cudaMemsetAsync(out->payload, 0, 8 * words, ctx.s);
+    if (e == cudaSuccess && nb)
+      e = cudaMemcpyAsync(out->ref, sc.at<uint64_t>(o_ref), 8 * nb, cudaMemcpyDeviceToDevice, ctx.s);
+    if (e == cudaSuccess && nrem)
+      e = cudaMemcpyAsync(out->rem, sc.at<uint64_t>(o_rem), 8 * nrem, cudaMemcpyDeviceToDevice, ctx.s);
+    if (e == cudaSuccess && nb)
+      e = launch_rle2delta_pack(src, B, nb, sc.at<uint64_t>(o_cwx), out->cw, out->payload, err, ctx.s);
+    if (e != cudaSuccess) {
+      release(ctx, out);
+      return cuda_status(e);
+    }
+    ms_status st = finish_output(ctx, out, err, nb ? sc.at<uint64_t>(o_cwx) + nb + 1 : nullptr);
+    if (st != MS_OK) release(ctx, out);
+    return st;
+  }
   if (fmt.format == MS_RLE) {  // staged through an uncompressed buffer
     uint64_t* tmp = (uint64_t*)ctx.alloc(8 * (n ? n : 1));
     if (!tmp) return MS_E_NOMEM;

@@ -93,6 +93,13 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
                                  uint64_t* slots, uint32_t slot_words, uint32_t* wk, uint64_t* cwx,
                                  uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err, cudaStream_t s);
 
+// direct morph RLE -> DELTA_BP{B} (morph.cu): per-run widths / bases / remainder, then (after the
+// width scan and the exact allocation) the steps ORed into the zeroed payload and cw
+cudaError_t launch_rle2delta_widths(const ColView& c, uint32_t B, uint64_t nb, uint32_t* wk, uint64_t* ref,
+                                    uint64_t* rem, cudaStream_t s);
+cudaError_t launch_rle2delta_pack(const ColView& c, uint32_t B, uint64_t nb, const uint64_t* cwx, uint32_t* cw,
+                                  uint64_t* payload, uint32_t* err, cudaStream_t s);
+
 // RLE run starts (exclusive prefix of lengths), validation against n
 cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
                               uint32_t* ticket, uint32_t* err, cudaStream_t s);
