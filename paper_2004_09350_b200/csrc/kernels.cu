@@ -415,10 +415,19 @@ __global__ void __launch_bounds__(kThreads) rle_count_kernel(const uint64_t* __r
   __shared__ uint32_t wsum[kThreads / 32];
   const uint64_t T = (n + kChunk - 1) / kChunk;
   for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    // rows t*kChunk + tid + q*kThreads (coalesced), all 16 loads in flight together
+    uint64_t a[kVPT], b[kVPT];
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      const uint64_t r = t * kChunk + threadIdx.x + q * kThreads;
+      a[q] = r < n ? __ldg(v + r) : 0ull;
+      b[q] = (r >= 1 && r < n) ? __ldg(v + r - 1) : ~a[q];
+    }
     uint32_t c = 0;
-    for (uint32_t i = threadIdx.x; i < kChunk; i += kThreads) {
-      const uint64_t r = t * kChunk + i;
-      if (r < n && (r == 0 || v[r] != v[r - 1])) ++c;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      const uint64_t r = t * kChunk + threadIdx.x + q * kThreads;
+      if (r < n && a[q] != b[q]) ++c;
     }
     c = (uint32_t)warp_sum(c);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
@@ -448,11 +457,17 @@ __global__ void __launch_bounds__(kThreads) rle_write_kernel(const uint64_t* __r
   const int tid = threadIdx.x;
   for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
     const uint64_t r0 = t * kChunk + tid * kVPT;
+    uint64_t x[kVPT + 1];
+#pragma unroll
+    for (int q = 0; q <= kVPT; ++q) {
+      const uint64_t r = r0 + q - 1;
+      x[q] = (r0 + q >= 1 && r < n) ? __ldg(v + r) : 0ull;
+    }
     uint32_t marks = 0, c = 0;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
       const uint64_t r = r0 + q;
-      if (r < n && (r == 0 || v[r] != v[r - 1])) {
+      if (r < n && (r == 0 || x[q + 1] != x[q])) {
         marks |= 1u << q;
         ++c;
       }
@@ -461,7 +476,7 @@ __global__ void __launch_bounds__(kThreads) rle_write_kernel(const uint64_t* __r
 #pragma unroll
     for (int q = 0; q < kVPT; ++q)
       if (marks & (1u << q)) {
-        payload[2 * idx] = v[r0 + q];
+        payload[2 * idx] = x[q + 1];
         starts[idx] = r0 + q;
         ++idx;
       }
