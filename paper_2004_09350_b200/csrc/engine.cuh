@@ -98,32 +98,59 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     sm.bmax[tid] = 0;
   }
   __syncthreads();
+  // codes (DELTA: in-block differences) and per-block min / max, rows lane-strided
+  // (tid + q * kThreads: conflict-free shared-memory access; a warp's 32 rows lie in
+  // one block, B >= 128); DELTA codes replace the values in place afterwards and the
+  // block bases are kept in bmin (unused by DELTA)
   {
-    const uint32_t i0 = tid * kVPT;
-    if (i0 < (nbc << lg)) {
-      const uint32_t blk = i0 >> lg;
-      uint64_t lmin = ~0ull, lmax = 0;
+    const uint32_t nmain = nbc << lg;
+    const uint32_t lane = tid & 31;
+    uint64_t cq[kVPT];
+    uint64_t lmin = ~0ull, lmax = 0;
+    uint32_t cur = ~0u;
+    auto flush = [&]() {
+      for (uint32_t sh = 16; sh > 0; sh >>= 1) {
+        const uint64_t a = __shfl_xor_sync(kFull, lmin, sh), b2 = __shfl_xor_sync(kFull, lmax, sh);
+        lmin = a < lmin ? a : lmin;
+        lmax = b2 > lmax ? b2 : lmax;
+      }
+      if (lane == 0) {
+        if (o.format == MS_FOR_BP) atomicMin((unsigned long long*)&sm.bmin[cur], (unsigned long long)lmin);
+        atomicMax((unsigned long long*)&sm.bmax[cur], (unsigned long long)lmax);
+      }
+      lmin = ~0ull;
+      lmax = 0;
+    };
 #pragma unroll
-      for (int q = 0; q < kVPT; ++q) {
-        const uint32_t j = i0 + q;
-        uint64_t c;
-        if (o.format == MS_DELTA_BP) c = (j & (B - 1)) ? sm.vals[j] - sm.vals[j - 1] : 0;
-        else c = sm.vals[j];
+    for (int q = 0; q < kVPT; ++q) {
+      const uint32_t j = tid + q * kThreads;
+      const uint32_t wrow = (tid & ~31u) + q * kThreads;  // the warp's first row at this step
+      uint64_t c = 0;
+      if (j < nmain) {
+        const uint64_t v = sm.vals[j];
+        if (o.format == MS_DELTA_BP) {
+          if (j & (B - 1)) c = v - sm.vals[j - 1];
+          else sm.bmin[j >> lg] = v;  // the block's base (D-6)
+        } else {
+          c = v;
+        }
+      }
+      cq[q] = c;
+      if (wrow < nmain) {
+        const uint32_t blk = wrow >> lg;
+        if (blk != cur && cur != ~0u) flush();
+        cur = blk;
         lmin = c < lmin ? c : lmin;
         lmax = c > lmax ? c : lmax;
       }
-      // reduce over the B/8 threads of the block inside the warp first (B >= 128:
-      // groups of >= 16 lanes), then one shared atomic per group
-      const uint32_t grp = (B / kVPT) < 32u ? (B / kVPT) : 32u;
-      const unsigned gm = grp == 32 ? kFull : (((1u << grp) - 1) << ((tid & 31) & ~(grp - 1)));
-      for (uint32_t sh = grp >> 1; sh > 0; sh >>= 1) {
-        const uint64_t a = __shfl_xor_sync(gm, lmin, sh), b = __shfl_xor_sync(gm, lmax, sh);
-        lmin = a < lmin ? a : lmin;
-        lmax = b > lmax ? b : lmax;
-      }
-      if (((tid & 31) & (grp - 1)) == 0) {
-        if (o.format == MS_FOR_BP) atomicMin((unsigned long long*)&sm.bmin[blk], (unsigned long long)lmin);
-        atomicMax((unsigned long long*)&sm.bmax[blk], (unsigned long long)lmax);
+    }
+    if (cur != ~0u) flush();
+    if (o.format == MS_DELTA_BP) {
+      __syncthreads();  // every value read before the codes overwrite them
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) {
+        const uint32_t j = tid + q * kThreads;
+        if (j < nmain) sm.vals[j] = cq[q];
       }
     }
   }
@@ -148,7 +175,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
       }
       sm.bex[lane] = E + incl - w;
       if (o.format == MS_FOR_BP) o.ref[kb0 + lane] = sm.bmin[lane];
-      if (o.format == MS_DELTA_BP) o.ref[kb0 + lane] = sm.vals[lane << lg];
+      if (o.format == MS_DELTA_BP) o.ref[kb0 + lane] = sm.bmin[lane];
     }
     if (item == 0 && lane == 0) o.cw[0] = 0;
   }
@@ -166,7 +193,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
       auto code = [&](uint32_t j) { return v[j] - rf; };
       for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
     } else if (o.format == MS_DELTA_BP) {
-      auto code = [&](uint32_t j) { return j ? v[j] - v[j - 1] : 0ull; };
+      auto code = [&](uint32_t j) { return v[j]; };  // the codes were written in place
       for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
     } else {
       auto code = [&](uint32_t j) { return v[j]; };
@@ -356,10 +383,18 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(Src src, OutView out, 
   __shared__ EngineSmem sm;
   const uint64_t n = out.n_dev ? *out.n_dev : out.n;
   const uint64_t n_items = (n + kChunk - 1) / kChunk;
+  // tiles in ticket order only when the output needs the look-back (block formats
+  // without slots); otherwise a static grid-stride order saves an atomic per tile
+  const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP ||
+                                      out.format == MS_DELTA_BP);
+  uint64_t next = blockIdx.x;
   while (true) {
-    if (threadIdx.x == 0) sm.item = atomicAdd(out.ticket, 1u);
-    __syncthreads();
-    const uint32_t item = sm.item;
+    if (ordered) {
+      if (threadIdx.x == 0) sm.item = atomicAdd(out.ticket, 1u);
+      __syncthreads();
+    }
+    const uint32_t item = ordered ? sm.item : (uint32_t)next;
+    next += gridDim.x;
     if (item >= n_items) break;
     const uint64_t r0 = (uint64_t)item * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
