@@ -290,7 +290,7 @@ __device__ __forceinline__ uint64_t read_row(const ColView& c, uint64_t r) {
 // -------------------------------------------------------- tile decoder
 // Shared memory of the generic engine.
 struct EngineSmem {
-  uint64_t vals[kChunk];
+  alignas(16) uint64_t vals[kChunk];
   uint64_t ex[kThreads];
   uint64_t scan[16];
   uint64_t bmin[kMaxBlocksPerChunk], bmax[kMaxBlocksPerChunk], bex[kMaxBlocksPerChunk];
@@ -299,6 +299,21 @@ struct EngineSmem {
   uint32_t flag;
   uint64_t aux;
 };
+
+// sm[0..8) = v[0..8) for thread-consecutive rows (thread t owns 8 rows at 64 t bytes):
+// four 128-bit stores, thread t starting at pair (t >> 1) & 3 so that the 8 threads
+// of a wavefront hit 8 distinct 16-byte bank groups (plain stores: 16-way conflicts)
+__device__ __forceinline__ void store8_rotated(uint64_t* sm, const uint64_t (&v)[kVPT]) {
+  static_assert(kVPT == 8, "store8_rotated assumes 8 rows per thread");
+  const uint32_t rot = (threadIdx.x >> 1) & 3;
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k) {
+    const uint32_t p = (k + rot) & 3;
+    const uint64_t a0 = (p & 1) ? v[2] : v[0], a1 = (p & 1) ? v[3] : v[1];
+    const uint64_t b0 = (p & 1) ? v[6] : v[4], b1 = (p & 1) ? v[7] : v[5];
+    reinterpret_cast<ulonglong2*>(sm)[p] = make_ulonglong2((p & 2) ? b0 : a0, (p & 2) ? b1 : a1);
+  }
+}
 
 // Decode rows [r0, r0+cnt) of column c into sm.vals (buffer layer, input side,
 // P:479-481). r0 is a multiple of kChunk (hence of every block size), cnt <= kChunk.
@@ -351,17 +366,28 @@ __device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_
       uint64_t loc[kVPT];
       uint64_t tsum = 0;
       const bool in_main = i0 < cnt && r < main_rows;
-      uint64_t b = 0;
+      uint64_t b = 0, ref_b = 0;
       if (in_main) {
         b = r >> c.log2B;
         const uint32_t j0 = (uint32_t)(r & (c.B - 1));
         const uint32_t cw0 = __ldg(c.cw + b);
         const uint32_t w = __ldg(c.cw + b + 1) - cw0;
-        const uint64_t bit0 = (uint64_t)cw0 * c.B + (uint64_t)j0 * w;
+        ref_b = __ldg(c.ref + b);  // issued with the header, used after the scan
+        // in-block bit positions in 32 bits (j * w < 2^17); the block starts word-aligned (B % 64 == 0)
+        const uint64_t* __restrict__ blk = c.payload + (uint64_t)cw0 * (c.B / 64);
+        const uint64_t mask = low_mask(w);
+        uint32_t pos = j0 * w;
 #pragma unroll
         for (int q = 0; q < kVPT; ++q) {
-          tsum += unpack_at(c.payload, bit0 + (uint64_t)q * w, w);
+          uint64_t x = 0;
+          if (w) {
+            const uint32_t wi = pos >> 6, sh = pos & 63;
+            x = __ldg(blk + wi) >> sh;
+            if (sh + w > 64) x |= __ldg(blk + wi + 1) << (64 - sh);
+          }
+          tsum += x & mask;
           loc[q] = tsum;
+          pos += w;
         }
       }
       const uint64_t ex = cta_excl_scan(in_main ? tsum : 0, sm.scan, nullptr);
@@ -369,9 +395,10 @@ __device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_
       __syncthreads();
       if (in_main) {
         const uint32_t head = (uint32_t)(((b << c.log2B) - r0) / kVPT);
-        const uint64_t base = __ldg(c.ref + b) + (ex - sm.ex[head]);
+        const uint64_t base = ref_b + (ex - sm.ex[head]);
 #pragma unroll
-        for (int q = 0; q < kVPT; ++q) sm.vals[i0 + q] = base + loc[q];
+        for (int q = 0; q < kVPT; ++q) loc[q] += base;
+        store8_rotated(sm.vals + i0, loc);
       } else {
         for (int q = 0; q < kVPT; ++q)
           if (i0 + q < cnt) sm.vals[i0 + q] = __ldg(c.rem + (r + q - main_rows));
@@ -383,7 +410,8 @@ __device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_
       const uint64_t k0 = __ldg(c.chunk_run + (r0 / kChunk));
       const uint32_t i0 = tid * kVPT;
       // reuse sm.vals as the mark array (1 = a run starts at this row, row > r0)
-      for (int q = 0; q < kVPT; ++q) sm.vals[i0 + q] = 0;
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) sm.vals[tid + q * kThreads] = 0;
       __syncthreads();
       for (uint64_t k = k0 + 1 + tid;; k += kThreads) {
         if (k >= c.nruns) break;
@@ -395,14 +423,22 @@ __device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_
       uint64_t loc[kVPT];
       uint64_t tsum = 0;
 #pragma unroll
-      for (int q = 0; q < kVPT; ++q) {
-        tsum += sm.vals[i0 + q];
+      for (int q = 0; q < kVPT; q += 2) {
+        const ulonglong2 m2 = reinterpret_cast<const ulonglong2*>(sm.vals + i0)[q / 2];
+        tsum += m2.x;
         loc[q] = tsum;
+        tsum += m2.y;
+        loc[q + 1] = tsum;
       }
       const uint64_t ex = cta_excl_scan(tsum, sm.scan, nullptr);
+      if (i0 + kVPT <= cnt) {
 #pragma unroll
-      for (int q = 0; q < kVPT; ++q)
-        if (i0 + q < cnt) sm.vals[i0 + q] = __ldg(c.payload + 2 * (k0 + ex + loc[q]));
+        for (int q = 0; q < kVPT; ++q) loc[q] = __ldg(c.payload + 2 * (k0 + ex + loc[q]));
+        store8_rotated(sm.vals + i0, loc);
+      } else {
+        for (int q = 0; q < kVPT; ++q)
+          if (i0 + q < cnt) sm.vals[i0 + q] = __ldg(c.payload + 2 * (k0 + ex + loc[q]));
+      }
       break;
     }
   }

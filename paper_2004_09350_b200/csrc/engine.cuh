@@ -58,7 +58,14 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
   const int tid = threadIdx.x;
   switch (o.format) {
     case MS_UNCOMPR:
-      for (uint32_t i = tid; i < cnt; i += kThreads) o.payload[r0 + i] = sm.vals[i];
+      if (cnt == kChunk && (reinterpret_cast<uintptr_t>(o.payload) & 15) == 0) {  // full tile: 128-bit stores
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(o.payload + r0);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(sm.vals);
+#pragma unroll
+        for (int q = 0; q < kVPT / 2; ++q) dst[tid + q * kThreads] = src[tid + q * kThreads];
+      } else {
+        for (uint32_t i = tid; i < cnt; i += kThreads) o.payload[r0 + i] = sm.vals[i];
+      }
       return;
     case MS_RLE:  // only for inputs without equal neighbours (select positions): runs of length 1
       for (uint32_t i = tid; i < cnt; i += kThreads) {
@@ -231,6 +238,7 @@ static __global__ void __launch_bounds__(256) tile_copy_kernel(OutView o, uint64
 // ------------------------------------------------------------------ sources
 // Decode of rows [r0, r0+cnt) of a column (compress / decompress / morph).
 struct ColSource {
+  static constexpr int kMinBlocks = 4;  // 64 registers: 4 CTAs per SM (latency-bound decode)
   ColView c;
   __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, EngineSmem& sm, uint32_t* err) const {
     load_rows(c, r0, cnt, sm);
@@ -240,6 +248,7 @@ struct ColSource {
 // Expansion of the select bit mask into positions (ranks r0 .. r0+cnt of the
 // output). Bit j of mask word m <=> row 32m + j matched.
 struct BitmaskSource {
+  static constexpr int kMinBlocks = 1;
   const uint32_t* bits;
   const uint64_t* seg_off;      // exclusive prefix of per-segment counts (segments of kSegRows rows)
   const uint32_t* start_seg;    // per output item: segment holding rank kChunk*item
@@ -277,6 +286,7 @@ struct BitmaskSource {
 // its positions, then all payload loads, so every thread has 8-16 independent
 // loads in flight instead of a dependent chain per position.
 struct GatherSource {
+  static constexpr int kMinBlocks = 1;
   ColView pos;
   ColView data;
   uint64_t row_offset;
@@ -379,7 +389,7 @@ struct GatherSource {
 };
 
 template <class Src>
-__global__ void __launch_bounds__(kThreads) engine_kernel(Src src, OutView out, uint32_t* err) {
+__global__ void __launch_bounds__(kThreads, Src::kMinBlocks) engine_kernel(Src src, OutView out, uint32_t* err) {
   __shared__ EngineSmem sm;
   const uint64_t n = out.n_dev ? *out.n_dev : out.n;
   const uint64_t n_items = (n + kChunk - 1) / kChunk;
@@ -388,6 +398,19 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(Src src, OutView out, 
   const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP ||
                                       out.format == MS_DELTA_BP);
   uint64_t next = blockIdx.x;
+  if (out.format == OUT_MAX_ONLY) {  // auto static width: a running max per thread, one atomic per warp at the end
+    uint64_t mx = 0;
+    for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const uint64_t r0 = item * kChunk;
+      const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
+      src.load((uint32_t)item, r0, cnt, sm, err);
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) mx = sm.vals[i] > mx ? sm.vals[i] : mx;
+      __syncthreads();
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(out.max_out, (unsigned long long)mx);
+    return;
+  }
   while (true) {
     if (ordered) {
       if (threadIdx.x == 0) sm.item = atomicAdd(out.ticket, 1u);

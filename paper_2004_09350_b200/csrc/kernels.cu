@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "engine.cuh"
+#include "stage.cuh"
 #include "grid.cuh"
 #include "launch.h"
 
@@ -108,6 +109,32 @@ static uint64_t n_items_hint(const OutView& o) {
 
 // ----------------------------------------------------------------- engine
 cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s) {
+  // staged input (stage.cuh) whenever tiles go in a static order: every output but
+  // a block format written with the look-back
+  const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP);
+  static const bool unstaged = getenv("MS_ENGINE_UNSTAGED") != nullptr;
+  // (an uncompressed source gains nothing: its direct loads are already independent)
+  if (stageable_format(src.format) && src.format != MS_UNCOMPR && !out.n_dev && !ordered && !unstaged) {
+    static bool attr[64] = {false};  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int dyn = (int)sizeof(StageSmem);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(engine_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_staged_kernel, kThreads, dyn);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t items = n_items_hint(out);
+    uint64_t g = (uint64_t)per_sm * num_sms();
+    if (items < g) g = items;
+    StagedCol sc{src, src.nb << src.log2B};
+    ProfScope prof_("engine_col", s);
+    engine_staged_kernel<<<(int)(g ? g : 1), kThreads, dyn, s>>>(sc, out, err);
+    return cudaGetLastError();
+  }
   auto k = engine_kernel<ColSource>;
   int grid = persistent_grid(k, kThreads, n_items_hint(out));
   ProfScope prof_("engine_col", s);

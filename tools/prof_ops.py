@@ -43,6 +43,16 @@ def c3():
     prof("select RLE", lambda: ms.select(R, ms.BETWEEN, 10**6, 2 * 10**6, out_fmt=ms.delta_bp(512)))
 
 
+def c3e():  # the engine ops of c3 only (for ncu: -k regex:engine_kernel)
+    n = 1 << 29
+    x = synth.gen_torch("c3.x", n)
+    D = ms.compress(x, ms.delta_bp(2048))
+    prof("compress DELTA_BP{2048}", lambda: ms.compress(x, ms.delta_bp(2048)), reps=1)
+    del x
+    prof("morph DELTA -> STATIC auto", lambda: ms.morph(D, ms.static_bp(0)), reps=1)
+    prof("decompress DELTA", lambda: ms.decompress(D), reps=1)
+
+
 def c4():
     n = 600_000_000
     Dm = synth.D4
