@@ -51,6 +51,20 @@ __device__ __forceinline__ uint64_t pack_word(CodeFn code, uint32_t cnt, uint32_
   return acc;
 }
 
+// The same for 32-bit output words (bits [32m, 32m+32)) when w <= 32: the codes'
+// low halves are enough and every step is one 32-bit instruction. Little-endian:
+// u32 word 2k (2k+1) is the low (high) half of u64 word k, so the stream is the same.
+__device__ __forceinline__ uint32_t pack_word32(const uint64_t* v, uint32_t cnt, uint32_t w, uint32_t mask, uint32_t m,
+                                                uint32_t magic, uint32_t sub = 0) {
+  const uint32_t* __restrict__ v32 = reinterpret_cast<const uint32_t*>(v);
+  const uint32_t bit0 = m * 32;
+  uint32_t j = div_small(bit0, w, magic);
+  uint32_t jb = j * w;
+  uint32_t acc = j < cnt ? ((v32[2 * j] - sub) & mask) >> (bit0 - jb) : 0u;
+  for (++j, jb += w; j < cnt && jb < bit0 + 32; ++j, jb += w) acc |= ((v32[2 * j] - sub) & mask) << (jb - bit0);
+  return acc;
+}
+
 // Output-side buffer layer: encode sm.vals[0..cnt) = rows
 // [r0, r0+cnt) of the output column. Item index = r0 / kChunk.
 __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uint64_t r0, uint32_t cnt,
@@ -87,9 +101,18 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
           if (sm.vals[i] >> w) atomicOr(err, err_bit(MS_E_WIDTH_OVERFLOW));
       const uint64_t mask = low_mask(w);
       const uint64_t wbase = (uint64_t)item * (kChunk / 64) * w;
+      const uint32_t magic = 0xffffffffu / w + 1u;
+      if (w <= 32) {
+        // u32 words; an odd count ends in the low half of the last u64 word, whose high
+        // half (no codes) is written 0 as the u64 path would
+        const uint32_t n32 = (cnt * w + 31) / 32, n32e = (n32 + 1) & ~1u;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(o.payload + wbase);
+        const uint32_t m32 = 0xffffffffu >> (32 - w);
+        for (uint32_t m = tid; m < n32e; m += kThreads) dst[m] = m < n32 ? pack_word32(sm.vals, cnt, w, m32, m, magic) : 0u;
+        return;
+      }
       const uint64_t nwords = ((uint64_t)cnt * w + 63) / 64;
       auto code = [&](uint32_t j) { return sm.vals[j] & mask; };
-      const uint32_t magic = 0xffffffffu / w + 1u;
       for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, cnt, w, m, magic);
       return;
     }
@@ -195,7 +218,12 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     const uint64_t wbase = sm.bex[bi] * (B / 64);
     const uint32_t nwords = (B / 64) * w;
     const uint32_t magic = 0xffffffffu / w + 1u;
-    if (o.format == MS_FOR_BP) {
+    if (w <= 32) {  // 32-bit words (B * w / 32 per block); FOR codes v - ref fit the low halves
+      uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + wbase);
+      const uint32_t m32 = 0xffffffffu >> (32 - w);
+      const uint32_t sub = o.format == MS_FOR_BP ? (uint32_t)sm.bmin[bi] : 0u;
+      for (uint32_t m = tid; m < 2 * nwords; m += kThreads) d32[m] = pack_word32(v, B, w, m32, m, magic, sub);
+    } else if (o.format == MS_FOR_BP) {
       const uint64_t rf = sm.bmin[bi];
       auto code = [&](uint32_t j) { return v[j] - rf; };
       for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
