@@ -293,7 +293,7 @@ struct EngineSmem {
   alignas(16) uint64_t vals[kChunk];
   uint64_t ex[kThreads];
   uint64_t scan[16];
-  uint64_t bmin[kMaxBlocksPerChunk], bmax[kMaxBlocksPerChunk], bex[kMaxBlocksPerChunk];
+  uint64_t bmin[kMaxBlocksPerChunk], bmax[kMaxBlocksPerChunk], bex[kMaxBlocksPerChunk + 1];
   uint32_t bw[kMaxBlocksPerChunk];
   uint32_t item;
   uint32_t flag;

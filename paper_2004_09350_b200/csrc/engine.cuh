@@ -123,33 +123,44 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
   const uint32_t B = o.B, lg = o.log2B;
   const uint32_t nbc = cnt >> lg;  // full blocks in this tile (all but the last tile: kChunk/B)
   const uint64_t kb0 = r0 >> lg;   // global index of the tile's first block
+  const bool is_for = o.format == MS_FOR_BP;
   if (tid < kMaxBlocksPerChunk) {
     sm.bmin[tid] = ~0ull;
     sm.bmax[tid] = 0;
+    sm.bw[tid] = 0;
   }
   __syncthreads();
-  // codes (DELTA: in-block differences) and per-block min / max, rows lane-strided
+  // codes (DELTA: in-block differences) and per-block widths, rows lane-strided
   // (tid + q * kThreads: conflict-free shared-memory access; a warp's 32 rows lie in
-  // one block, B >= 128); DELTA codes replace the values in place afterwards and the
-  // block bases are kept in bmin (unused by DELTA)
+  // one block, B >= 128). DYN / DELTA: w_b = max ebw(code) by one 32-bit warp
+  // reduction (redux.sync) per block run; FOR: 64-bit min and max, each as two
+  // 32-bit reductions (high halves, then low halves of the lanes at the high max).
+  // DELTA codes replace the values in place afterwards; the block bases are kept in
+  // bmin (unused by DELTA).
   {
     const uint32_t nmain = nbc << lg;
     const uint32_t lane = tid & 31;
     uint64_t cq[kVPT];
     uint64_t lmin = ~0ull, lmax = 0;
+    uint32_t lw = 0;
     uint32_t cur = ~0u;
     auto flush = [&]() {
-      for (uint32_t sh = 16; sh > 0; sh >>= 1) {
-        const uint64_t a = __shfl_xor_sync(kFull, lmin, sh), b2 = __shfl_xor_sync(kFull, lmax, sh);
-        lmin = a < lmin ? a : lmin;
-        lmax = b2 > lmax ? b2 : lmax;
-      }
-      if (lane == 0) {
-        if (o.format == MS_FOR_BP) atomicMin((unsigned long long*)&sm.bmin[cur], (unsigned long long)lmin);
-        atomicMax((unsigned long long*)&sm.bmax[cur], (unsigned long long)lmax);
+      if (is_for) {
+        const uint32_t hmax = __reduce_max_sync(kFull, (uint32_t)(lmax >> 32));
+        const uint32_t lmx = __reduce_max_sync(kFull, (uint32_t)(lmax >> 32) == hmax ? (uint32_t)lmax : 0u);
+        const uint32_t hmin = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32));
+        const uint32_t lmn = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32) == hmin ? (uint32_t)lmin : ~0u);
+        if (lane == 0) {
+          atomicMin((unsigned long long*)&sm.bmin[cur], ((unsigned long long)hmin << 32) | lmn);
+          atomicMax((unsigned long long*)&sm.bmax[cur], ((unsigned long long)hmax << 32) | lmx);
+        }
+      } else {
+        const uint32_t wm = __reduce_max_sync(kFull, lw);
+        if (lane == 0 && wm) atomicMax(&sm.bw[cur], wm);
       }
       lmin = ~0ull;
       lmax = 0;
+      lw = 0;
     };
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
@@ -170,8 +181,13 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
         const uint32_t blk = wrow >> lg;
         if (blk != cur && cur != ~0u) flush();
         cur = blk;
-        lmin = c < lmin ? c : lmin;
-        lmax = c > lmax ? c : lmax;
+        if (is_for) {
+          lmin = c < lmin ? c : lmin;
+          lmax = c > lmax ? c : lmax;
+        } else {
+          const uint32_t e = ebw64(c);
+          lw = e > lw ? e : lw;
+        }
       }
     }
     if (cur != ~0u) flush();
@@ -189,7 +205,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     const int lane = tid;
     uint32_t w = 0;
     if (lane < (int)nbc) {
-      w = o.format == MS_FOR_BP ? ebw64(sm.bmax[lane] - sm.bmin[lane]) : ebw64(sm.bmax[lane]);
+      w = is_for ? ebw64(sm.bmax[lane] - sm.bmin[lane]) : sm.bw[lane];
       sm.bw[lane] = w;
     }
     const uint64_t incl = warp_incl_scan(w);
@@ -204,35 +220,46 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
         o.cw[kb0 + lane + 1] = (uint32_t)c_incl;
       }
       sm.bex[lane] = E + incl - w;
-      if (o.format == MS_FOR_BP) o.ref[kb0 + lane] = sm.bmin[lane];
-      if (o.format == MS_DELTA_BP) o.ref[kb0 + lane] = sm.bmin[lane];
+      if (is_for || o.format == MS_DELTA_BP) o.ref[kb0 + lane] = sm.bmin[lane];
     }
+    if (lane == (int)nbc) sm.bex[lane] = E + tile_sum;  // end of the tile's last block
     if (item == 0 && lane == 0) o.cw[0] = 0;
   }
   __syncthreads();
-  for (uint32_t bi = 0; bi < nbc; ++bi) {
-    const uint32_t w = sm.bw[bi];
-    if (w == 0) continue;
-    const uint64_t* v = sm.vals + (bi << lg);
-    uint64_t* const dst = o.slots ? o.slots + (uint64_t)item * kChunk : o.payload;  // tile slot or final place
-    const uint64_t wbase = sm.bex[bi] * (B / 64);
-    const uint32_t nwords = (B / 64) * w;
-    const uint32_t magic = 0xffffffffu / w + 1u;
-    if (w <= 32) {  // 32-bit words (B * w / 32 per block); FOR codes v - ref fit the low halves
-      uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + wbase);
-      const uint32_t m32 = 0xffffffffu >> (32 - w);
-      const uint32_t sub = o.format == MS_FOR_BP ? (uint32_t)sm.bmin[bi] : 0u;
-      for (uint32_t m = tid; m < 2 * nwords; m += kThreads) d32[m] = pack_word32(v, B, w, m32, m, magic, sub);
-    } else if (o.format == MS_FOR_BP) {
-      const uint64_t rf = sm.bmin[bi];
-      auto code = [&](uint32_t j) { return v[j] - rf; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
-    } else if (o.format == MS_DELTA_BP) {
-      auto code = [&](uint32_t j) { return v[j]; };  // the codes were written in place
-      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
-    } else {
-      auto code = [&](uint32_t j) { return v[j]; };
-      for (uint32_t m = tid; m < nwords; m += kThreads) dst[wbase + m] = pack_word(code, B, w, m, magic);
+  // pack: the tile's blocks are consecutive in the output, so its u64 words are one
+  // flat range [0, (bex[nbc] - bex[0]) * B / 64) over all threads; word m belongs to
+  // the block whose range holds it (a cursor that only moves forward)
+  if (nbc) {
+    const uint64_t e0 = sm.bex[0];
+    const uint32_t wpb = B / 64;  // u64 words per unit of width
+    const uint32_t total = (uint32_t)(sm.bex[nbc] - e0) * wpb;
+    uint64_t* const dst = (o.slots ? o.slots + (uint64_t)item * kChunk : o.payload) + e0 * wpb;
+    uint32_t bi = 0, bstart = 0, bend = (uint32_t)(sm.bex[1] - e0) * wpb;
+    for (uint32_t m = tid; m < total; m += kThreads) {
+      while (m >= bend) {
+        ++bi;
+        bstart = bend;
+        bend = (uint32_t)(sm.bex[bi + 1] - e0) * wpb;
+      }
+      const uint32_t w = sm.bw[bi];
+      const uint32_t magic = 0xffffffffu / w + 1u;
+      const uint64_t* v = sm.vals + (bi << lg);
+      const uint32_t mb = m - bstart;  // word within the block
+      uint64_t word;
+      if (w <= 32) {  // two 32-bit words; FOR codes v - ref fit the low halves
+        const uint32_t m32 = 0xffffffffu >> (32 - w);
+        const uint32_t sub = is_for ? (uint32_t)sm.bmin[bi] : 0u;
+        word = (uint64_t)pack_word32(v, B, w, m32, 2 * mb, magic, sub) |
+               ((uint64_t)pack_word32(v, B, w, m32, 2 * mb + 1, magic, sub) << 32);
+      } else if (is_for) {
+        const uint64_t rf = sm.bmin[bi];
+        auto code = [&](uint32_t j) { return v[j] - rf; };
+        word = pack_word(code, B, w, mb, magic);
+      } else {
+        auto code = [&](uint32_t j) { return v[j]; };  // DELTA: the codes were written in place
+        word = pack_word(code, B, w, mb, magic);
+      }
+      dst[m] = word;
     }
   }
   const uint32_t rem_cnt = cnt - (nbc << lg);
@@ -314,7 +341,7 @@ struct BitmaskSource {
 // its positions, then all payload loads, so every thread has 8-16 independent
 // loads in flight instead of a dependent chain per position.
 struct GatherSource {
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = 2;  // <= 128 registers (unbounded: 190, one CTA per SM)
   ColView pos;
   ColView data;
   uint64_t row_offset;

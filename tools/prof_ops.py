@@ -53,6 +53,14 @@ def c3e():  # the engine ops of c3 only (for ncu: -k regex:engine_kernel)
     prof("decompress DELTA", lambda: ms.decompress(D), reps=1)
 
 
+def c2e():  # compress of c2's X (UNCOMPR -> DYN_BP{512}) only (for ncu: -k regex:engine_kernel)
+    n = 1 << 28
+    x = synth.gen_torch("c2.X", n)
+    prof("compress c2.X -> DYN_BP{512}", lambda: ms.compress(x, ms.dyn_bp(512)), reps=1)
+    prof("compress c2.X -> FOR_BP{512}", lambda: ms.compress(x, ms.for_bp(512)), reps=1)
+    prof("compress c2.X -> STATIC_BP{auto}", lambda: ms.compress(x, ms.static_bp(0)), reps=1)
+
+
 def c4():
     n = 600_000_000
     Dm = synth.D4
