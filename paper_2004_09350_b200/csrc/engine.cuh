@@ -67,29 +67,30 @@ __device__ __forceinline__ uint32_t pack_word32(const uint64_t* v, uint32_t cnt,
 
 // Output-side buffer layer: encode sm.vals[0..cnt) = rows
 // [r0, r0+cnt) of the output column. Item index = r0 / kChunk.
+// vals: the tile's rows (sm.vals, or a staged input buffer encoded in place)
 __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uint64_t r0, uint32_t cnt,
-                                            uint64_t n, EngineSmem& sm, uint32_t* err) {
+                                            uint64_t n, EngineSmem& sm, uint32_t* err, uint64_t* vals) {
   const int tid = threadIdx.x;
   switch (o.format) {
     case MS_UNCOMPR:
       if (cnt == kChunk && (reinterpret_cast<uintptr_t>(o.payload) & 15) == 0) {  // full tile: 128-bit stores
         ulonglong2* dst = reinterpret_cast<ulonglong2*>(o.payload + r0);
-        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(sm.vals);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(vals);
 #pragma unroll
         for (int q = 0; q < kVPT / 2; ++q) dst[tid + q * kThreads] = src[tid + q * kThreads];
       } else {
-        for (uint32_t i = tid; i < cnt; i += kThreads) o.payload[r0 + i] = sm.vals[i];
+        for (uint32_t i = tid; i < cnt; i += kThreads) o.payload[r0 + i] = vals[i];
       }
       return;
     case MS_RLE:  // only for inputs without equal neighbours (select positions): runs of length 1
       for (uint32_t i = tid; i < cnt; i += kThreads) {
-        o.payload[2 * (r0 + i)] = sm.vals[i];
+        o.payload[2 * (r0 + i)] = vals[i];
         o.payload[2 * (r0 + i) + 1] = 1;
       }
       return;
     case OUT_MAX_ONLY: {
       uint64_t mx = 0;
-      for (uint32_t i = tid; i < cnt; i += kThreads) mx = sm.vals[i] > mx ? sm.vals[i] : mx;
+      for (uint32_t i = tid; i < cnt; i += kThreads) mx = vals[i] > mx ? vals[i] : mx;
       mx = warp_max(mx);
       if ((tid & 31) == 0 && mx) atomicMax(o.max_out, (unsigned long long)mx);
       return;
@@ -98,7 +99,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
       const uint32_t w = o.w;
       if (w < 64)
         for (uint32_t i = tid; i < cnt; i += kThreads)
-          if (sm.vals[i] >> w) atomicOr(err, err_bit(MS_E_WIDTH_OVERFLOW));
+          if (vals[i] >> w) atomicOr(err, err_bit(MS_E_WIDTH_OVERFLOW));
       const uint64_t mask = low_mask(w);
       const uint64_t wbase = (uint64_t)item * (kChunk / 64) * w;
       const uint32_t magic = 0xffffffffu / w + 1u;
@@ -108,11 +109,11 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
         const uint32_t n32 = (cnt * w + 31) / 32, n32e = (n32 + 1) & ~1u;
         uint32_t* dst = reinterpret_cast<uint32_t*>(o.payload + wbase);
         const uint32_t m32 = 0xffffffffu >> (32 - w);
-        for (uint32_t m = tid; m < n32e; m += kThreads) dst[m] = m < n32 ? pack_word32(sm.vals, cnt, w, m32, m, magic) : 0u;
+        for (uint32_t m = tid; m < n32e; m += kThreads) dst[m] = m < n32 ? pack_word32(vals, cnt, w, m32, m, magic) : 0u;
         return;
       }
       const uint64_t nwords = ((uint64_t)cnt * w + 63) / 64;
-      auto code = [&](uint32_t j) { return sm.vals[j] & mask; };
+      auto code = [&](uint32_t j) { return vals[j] & mask; };
       for (uint32_t m = tid; m < nwords; m += kThreads) o.payload[wbase + m] = pack_word(code, cnt, w, m, magic);
       return;
     }
@@ -168,9 +169,9 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
       const uint32_t wrow = (tid & ~31u) + q * kThreads;  // the warp's first row at this step
       uint64_t c = 0;
       if (j < nmain) {
-        const uint64_t v = sm.vals[j];
+        const uint64_t v = vals[j];
         if (o.format == MS_DELTA_BP) {
-          if (j & (B - 1)) c = v - sm.vals[j - 1];
+          if (j & (B - 1)) c = v - vals[j - 1];
           else sm.bmin[j >> lg] = v;  // the block's base (D-6)
         } else {
           c = v;
@@ -196,7 +197,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
 #pragma unroll
       for (int q = 0; q < kVPT; ++q) {
         const uint32_t j = tid + q * kThreads;
-        if (j < nmain) sm.vals[j] = cq[q];
+        if (j < nmain) vals[j] = cq[q];
       }
     }
   }
@@ -243,7 +244,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
       }
       const uint32_t w = sm.bw[bi];
       const uint32_t magic = 0xffffffffu / w + 1u;
-      const uint64_t* v = sm.vals + (bi << lg);
+      const uint64_t* v = vals + (bi << lg);
       const uint32_t mb = m - bstart;  // word within the block
       uint64_t word;
       if (w <= 32) {  // two 32-bit words; FOR codes v - ref fit the low halves
@@ -264,7 +265,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
   }
   const uint32_t rem_cnt = cnt - (nbc << lg);
   if (rem_cnt) {  // the final partial block -> uncompressed remainder
-    for (uint32_t i = tid; i < rem_cnt; i += kThreads) o.rem[i] = sm.vals[(nbc << lg) + i];
+    for (uint32_t i = tid; i < rem_cnt; i += kThreads) o.rem[i] = vals[(nbc << lg) + i];
   }
 }
 
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, Src::kMinBlocks) engine_kernel(Src s
     const uint64_t r0 = (uint64_t)item * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
     src.load(item, r0, cnt, sm, err);
-    encode_tile(out, item, r0, cnt, n, sm, err);
+    encode_tile(out, item, r0, cnt, n, sm, err, sm.vals);
     __syncthreads();
   }
 }

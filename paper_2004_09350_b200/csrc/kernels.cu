@@ -113,8 +113,7 @@ cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* 
   // a block format written with the look-back
   const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP);
   static const bool unstaged = getenv("MS_ENGINE_UNSTAGED") != nullptr;
-  // (an uncompressed source gains nothing: its direct loads are already independent)
-  if (stageable_format(src.format) && src.format != MS_UNCOMPR && !out.n_dev && !ordered && !unstaged) {
+  if (stageable_format(src.format) && !out.n_dev && !ordered && !unstaged) {
     static bool attr[64] = {false};  // per device
     int dev = 0;
     cudaGetDevice(&dev);

@@ -251,11 +251,15 @@ __global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol sr
     st_commit();
     const uint64_t r0 = t * kChunk;
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
-    src.decode(t, cnt, st, buf, slot, sm);
+    // an uncompressed source is encoded straight from its staging buffer (r0 is even:
+    // no word offset)
+    uint64_t* vals = sm.vals;
+    if (src.c.format == MS_UNCOMPR) vals = st.words[buf];
+    else src.decode(t, cnt, st, buf, slot, sm);
     if (out.format == OUT_MAX_ONLY) {
-      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) mx = sm.vals[i] > mx ? sm.vals[i] : mx;
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) mx = vals[i] > mx ? vals[i] : mx;
     } else {
-      encode_tile(out, (uint32_t)t, r0, cnt, n, sm, err);
+      encode_tile(out, (uint32_t)t, r0, cnt, n, sm, err, vals);
     }
     __syncthreads();
   }
