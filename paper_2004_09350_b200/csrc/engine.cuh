@@ -236,14 +236,17 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     const uint32_t total = (uint32_t)(sm.bex[nbc] - e0) * wpb;
     uint64_t* const dst = (o.slots ? o.slots + (uint64_t)item * kChunk : o.payload) + e0 * wpb;
     uint32_t bi = 0, bstart = 0, bend = (uint32_t)(sm.bex[1] - e0) * wpb;
+    uint32_t w = sm.bw[0], magic = w ? 0xffffffffu / w + 1u : 0u;
     for (uint32_t m = tid; m < total; m += kThreads) {
-      while (m >= bend) {
-        ++bi;
-        bstart = bend;
-        bend = (uint32_t)(sm.bex[bi + 1] - e0) * wpb;
+      if (m >= bend) {
+        while (m >= bend) {
+          ++bi;
+          bstart = bend;
+          bend = (uint32_t)(sm.bex[bi + 1] - e0) * wpb;
+        }
+        w = sm.bw[bi];
+        magic = 0xffffffffu / w + 1u;  // w > 0: the block has words
       }
-      const uint32_t w = sm.bw[bi];
-      const uint32_t magic = 0xffffffffu / w + 1u;
       const uint64_t* v = vals + (bi << lg);
       const uint32_t mb = m - bstart;  // word within the block
       uint64_t word;

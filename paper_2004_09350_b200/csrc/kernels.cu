@@ -114,24 +114,26 @@ cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* 
   const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP);
   static const bool unstaged = getenv("MS_ENGINE_UNSTAGED") != nullptr;
   if (stageable_format(src.format) && !out.n_dev && !ordered && !unstaged) {
-    static bool attr[64] = {false};  // per device
+    static bool attr[64][2] = {};  // per device and instantiation
     int dev = 0;
     cudaGetDevice(&dev);
+    const bool max_only = out.format == OUT_MAX_ONLY;
+    auto k = max_only ? engine_staged_kernel<true> : engine_staged_kernel<false>;
     const int dyn = (int)sizeof(StageSmem);
-    if (dev < 0 || dev >= 64 || !attr[dev]) {
-      cudaError_t e = cudaFuncSetAttribute(engine_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (dev < 0 || dev >= 64 || !attr[dev][max_only]) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
       if (e != cudaSuccess) return e;
-      if (dev >= 0 && dev < 64) attr[dev] = true;
+      if (dev >= 0 && dev < 64) attr[dev][max_only] = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_staged_kernel, kThreads, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
     if (per_sm < 1) per_sm = 1;
     const uint64_t items = n_items_hint(out);
     uint64_t g = (uint64_t)per_sm * num_sms();
     if (items < g) g = items;
     StagedCol sc{src, src.nb << src.log2B};
     ProfScope prof_("engine_col", s);
-    engine_staged_kernel<<<(int)(g ? g : 1), kThreads, dyn, s>>>(sc, out, err);
+    k<<<(int)(g ? g : 1), kThreads, dyn, s>>>(sc, out, err);
     return cudaGetLastError();
   }
   auto k = engine_kernel<ColSource>;

@@ -22,6 +22,7 @@ struct StageSmem {
   alignas(16) uint64_t words[2][kChunk + 2];  // <= 2048 words per tile (64 bits per row) + alignment
   uint32_t cw[3][kMaxBlocksPerChunk + 1];
   uint64_t ref[3][kMaxBlocksPerChunk];
+  uint32_t off[2];  // word offset of the tile's first word in words[buf] (16-byte copies)
 };
 
 __device__ __forceinline__ void st_cp8(void* smem, const void* gmem) {
@@ -93,8 +94,10 @@ struct StagedCol {
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
     uint64_t lo, hi;
     range(t, cnt, st, slot, lo, hi);
+    const bool al16 = (reinterpret_cast<uintptr_t>(c.payload) & 15) == 0;
+    if (threadIdx.x == 0) st.off[buf] = al16 ? (uint32_t)(lo & 1) : 0u;  // read after the next barrier
     if (hi <= lo) return;
-    if ((reinterpret_cast<uintptr_t>(c.payload) & 15) == 0) {
+    if (al16) {
       const uint64_t base = lo & ~1ull;
       const uint32_t nw = (uint32_t)(hi - base), npair = nw >> 1;
       const ulonglong2* src = reinterpret_cast<const ulonglong2*>(c.payload + base);
@@ -104,25 +107,24 @@ struct StagedCol {
       for (uint32_t i = threadIdx.x; i < (uint32_t)(hi - lo); i += kThreads) st_cp8(&st.words[buf][i], c.payload + lo + i);
     }
   }
-  __device__ __forceinline__ uint32_t word_off(uint64_t t, uint32_t cnt, const StageSmem& st, int slot) const {
-    if ((reinterpret_cast<uintptr_t>(c.payload) & 15) != 0) return 0;
-    uint64_t lo, hi;
-    range(t, cnt, st, slot, lo, hi);
-    return (uint32_t)(lo & 1);
-  }
-
-  // rows [r0, r0 + cnt) of tile t from the staged words into sm.vals; ends with a barrier
+  // rows [r0, r0 + cnt) of tile t from the staged words into sm.vals (ends with a
+  // barrier), or, kMaxOnly, only their running maximum in mx (no stores, no barrier)
+  template <bool kMaxOnly>
   __device__ __forceinline__ void decode(uint64_t t, uint32_t cnt, const StageSmem& st, int buf, int slot,
-                                         EngineSmem& sm) const {
+                                         EngineSmem& sm, uint64_t& mx) const {
     const int tid = threadIdx.x;
     const uint64_t r0 = t * kChunk;
-    const uint64_t* __restrict__ wd = st.words[buf] + word_off(t, cnt, st, slot);
+    const uint64_t* __restrict__ wd = st.words[buf] + st.off[buf];
+    auto put = [&](uint32_t i, uint64_t v) {
+      if (kMaxOnly) mx = v > mx ? v : mx;
+      else sm.vals[i] = v;
+    };
     switch (c.format) {
       case MS_UNCOMPR:
 #pragma unroll
         for (int q = 0; q < kVPT; ++q) {
           const uint32_t i = tid + q * kThreads;
-          if (i < cnt) sm.vals[i] = wd[i];
+          if (i < cnt) put(i, wd[i]);
         }
         break;
       case MS_STATIC_BP: {
@@ -135,7 +137,7 @@ struct StagedCol {
             const uint32_t pos = i * w, wi = pos >> 6, sh = pos & 63;
             uint64_t x = wd[wi] >> sh;
             if (sh + w > 64) x |= wd[wi + 1] << (64 - sh);
-            sm.vals[i] = x & mask;
+            put(i, x & mask);
           }
         }
         break;
@@ -157,9 +159,9 @@ struct StagedCol {
               if (sh + w > 64) x |= wd[wi + 1] << (64 - sh);
               x &= low_mask(w);
             }
-            sm.vals[i] = c.format == MS_FOR_BP ? st.ref[slot][b] + x : x;
+            put(i, c.format == MS_FOR_BP ? st.ref[slot][b] + x : x);
           } else if (i < cnt) {
-            sm.vals[i] = __ldg(c.rem + (r0 + i - main_rows));
+            put(i, __ldg(c.rem + (r0 + i - main_rows)));
           }
         }
         break;
@@ -210,18 +212,25 @@ struct StagedCol {
           const uint64_t base = st.ref[slot][b] + (ex - sm.ex[head]);
 #pragma unroll
           for (int q = 0; q < kVPT; ++q) loc[q] += base;
-          store8_rotated(sm.vals + i0, loc);
+          if (kMaxOnly) {
+#pragma unroll
+            for (int q = 0; q < kVPT; ++q) mx = loc[q] > mx ? loc[q] : mx;
+          } else {
+            store8_rotated(sm.vals + i0, loc);
+          }
         } else {
           for (int q = 0; q < kVPT; ++q)
-            if (i0 + q < cnt) sm.vals[i0 + q] = __ldg(c.rem + (r0 + i0 + q - main_rows));
+            if (i0 + q < cnt) put(i0 + q, __ldg(c.rem + (r0 + i0 + q - main_rows)));
         }
         break;
       }
     }
-    __syncthreads();
+    if (!kMaxOnly) __syncthreads();
   }
 };
 
+// kMaxOnly: the auto-static-width pre-pass (OUT_MAX_ONLY), its own instantiation
+template <bool kMaxOnly>
 __global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol src, OutView out, uint32_t* err) {
   __shared__ EngineSmem sm;
   extern __shared__ __align__(16) unsigned char st_raw[];
@@ -253,17 +262,17 @@ __global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol sr
     const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, n - r0);
     // an uncompressed source is encoded straight from its staging buffer (r0 is even:
     // no word offset)
-    uint64_t* vals = sm.vals;
-    if (src.c.format == MS_UNCOMPR) vals = st.words[buf];
-    else src.decode(t, cnt, st, buf, slot, sm);
-    if (out.format == OUT_MAX_ONLY) {
-      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) mx = vals[i] > mx ? vals[i] : mx;
+    if (kMaxOnly) {  // auto static width: decode straight into a running max
+      src.decode<true>(t, cnt, st, buf, slot, sm, mx);
     } else {
+      uint64_t* vals = sm.vals;
+      if (src.c.format == MS_UNCOMPR) vals = st.words[buf];
+      else src.decode<false>(t, cnt, st, buf, slot, sm, mx);
       encode_tile(out, (uint32_t)t, r0, cnt, n, sm, err, vals);
     }
     __syncthreads();
   }
-  if (out.format == OUT_MAX_ONLY) {
+  if (kMaxOnly) {
     mx = warp_max(mx);
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(out.max_out, (unsigned long long)mx);
   }
