@@ -477,37 +477,57 @@ cudaError_t launch_rle_count(const uint64_t* v, uint64_t n, uint32_t* counts, cu
   return cudaGetLastError();
 }
 
+// rows lane-strided (t*kChunk + tid + q*kThreads: coalesced, as rle_count); a run
+// start's rank inside the tile = the starts of earlier (step, warp) groups (a scan
+// over the 8 x 8 ballot counts) + the earlier lanes of its own ballot
 __global__ void __launch_bounds__(kThreads) rle_write_kernel(const uint64_t* __restrict__ v, uint64_t n,
                                                              const uint64_t* chunk_off, uint64_t* payload,
                                                              uint64_t* starts) {
-  __shared__ uint64_t scan_sm[16];
+  constexpr int kWarps = kThreads / 32;
+  static_assert(kVPT * kWarps == 64, "two ballot counts per lane of one warp");
+  __shared__ uint32_t grp[kVPT * kWarps];  // counts, then exclusive offsets, of (step q, warp w) at q*kWarps+w
   const uint64_t T = (n + kChunk - 1) / kChunk;
   const int tid = threadIdx.x;
+  const uint32_t lane = tid & 31, wid = tid >> 5;
   for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
-    const uint64_t r0 = t * kChunk + tid * kVPT;
-    uint64_t x[kVPT + 1];
-#pragma unroll
-    for (int q = 0; q <= kVPT; ++q) {
-      const uint64_t r = r0 + q - 1;
-      x[q] = (r0 + q >= 1 && r < n) ? __ldg(v + r) : 0ull;
-    }
-    uint32_t marks = 0, c = 0;
+    uint64_t a[kVPT], b[kVPT];
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
-      const uint64_t r = r0 + q;
-      if (r < n && (r == 0 || x[q + 1] != x[q])) {
-        marks |= 1u << q;
-        ++c;
-      }
+      const uint64_t r = t * kChunk + tid + q * kThreads;
+      a[q] = r < n ? __ldg(v + r) : 0ull;
+      b[q] = (r >= 1 && r < n) ? __ldg(v + r - 1) : ~a[q];
     }
-    uint64_t idx = chunk_off[t] + cta_excl_scan(c, scan_sm, nullptr);
+    uint32_t bal[kVPT];
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      const uint64_t r = t * kChunk + tid + q * kThreads;
+      bal[q] = __ballot_sync(kFull, r < n && a[q] != b[q]);
+      if (lane == 0) grp[q * kWarps + wid] = __popc(bal[q]);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const uint32_t c0 = grp[2 * tid], c1 = grp[2 * tid + 1];
+      uint32_t x = c0 + c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if ((int)lane >= o) x += y;
+      }
+      const uint32_t ex = x - c0 - c1;
+      grp[2 * tid] = ex;
+      grp[2 * tid + 1] = ex + c0;
+    }
+    __syncthreads();
+    const uint64_t off = chunk_off[t];
+    const uint32_t below = (1u << lane) - 1u;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q)
-      if (marks & (1u << q)) {
-        payload[2 * idx] = x[q + 1];
-        starts[idx] = r0 + q;
-        ++idx;
+      if ((bal[q] >> lane) & 1u) {
+        const uint64_t idx = off + grp[q * kWarps + wid] + __popc(bal[q] & below);
+        payload[2 * idx] = a[q];
+        starts[idx] = t * kChunk + tid + q * kThreads;
       }
+    __syncthreads();  // grp is rewritten by the next tile
   }
 }
 

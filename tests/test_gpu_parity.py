@@ -82,6 +82,24 @@ def test_morph_pairs(kind, rng):
                 assert_same_image(gm, O.morph(oa, *oracle_fmt(b)), f"morph {a}->{b} {kind} n={n}")
 
 
+@pytest.mark.parametrize("kind", ["small", "sorted", "runs", "outlier", "wide"])
+def test_many_tiles_per_cta(kind, rng):
+    """More 2048-row tiles than resident CTAs (148 SMs x 4): the staged engine's
+    double-buffered pipeline runs several iterations per CTA, with a ragged tail."""
+    ms = get_ms()
+    n = (1 << 21) + 12_345
+    v = rand_values(n, kind, rng)
+    t = to_torch(v)
+    fm = [ms.static_bp(0), ms.dyn_bp(512), ms.for_bp(128), ms.delta_bp(2048), ms.delta_bp(256), ms.rle()]
+    for a in fm:
+        oa = O.encode(v, *oracle_fmt(a))
+        ga = ms.compress(t, a)
+        assert_same_image(ga, oa, f"compress {a} {kind} n={n}")
+        assert np.array_equal(ms.to_u64_numpy(ms.decompress(ga)), v), f"decompress {a} {kind}"
+        for b in (ms.static_bp(0), ms.delta_bp(512), ms.for_bp(2048), ms.uncompr()):
+            assert_same_image(ms.morph(ga, b), O.morph(oa, *oracle_fmt(b)), f"morph {a}->{b} {kind} n={n}")
+
+
 PREDS = None
 
 
