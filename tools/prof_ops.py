@@ -51,6 +51,9 @@ def c3e():  # the engine ops of c3 only (for ncu: -k regex:engine_kernel)
     del x
     prof("morph DELTA -> STATIC auto", lambda: ms.morph(D, ms.static_bp(0)), reps=1)
     prof("decompress DELTA", lambda: ms.decompress(D), reps=1)
+    R = ms.morph(D, ms.rle())
+    prof("decompress RLE", lambda: ms.decompress(R), reps=1)
+    prof("morph RLE -> DYN_BP{512}", lambda: ms.morph(R, ms.dyn_bp(512)), reps=1)
 
 
 def c2e():  # compress of c2's X (UNCOMPR -> DYN_BP{512}) only (for ncu: -k regex:engine_kernel)
