@@ -200,6 +200,38 @@ struct ProjectSource {
           if (i < cnt) P[pidx(i)] = v[q];
         }
       }
+    } else if (data.format == MS_STATIC_BP || data.format == MS_UNCOMPR) {
+      // O(1) addresses (bit r * w): a bulk L2 prefetch of the window between the
+      // first and last position (sorted positions; at most kStaticWindow bytes),
+      // then BATCH independent loads in flight per lane
+      constexpr uint64_t kStaticWindow = 32768;
+      const uint32_t w = data.format == MS_STATIC_BP ? data.w : 64u;
+      const uint64_t p_first = P[pidx(0)], p_last = P[pidx(cnt - 1)];
+      if (prefetch && lane == 0 && p_first >= row_offset && p_last >= p_first && p_last - row_offset < data.n) {
+        const uint64_t a_lo = (((p_first - row_offset) * w) >> 6) & ~1ull;  // 16-byte aligned word
+        const uint64_t a_hi = (((p_last - row_offset + 1) * w + 63) >> 6);
+        const uint64_t bytes = ((a_hi - a_lo) * 8) & ~15ull;
+        if (bytes >= 16 && bytes <= kStaticWindow)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(data.payload + a_lo), "r"((uint32_t)bytes)
+                       : "memory");
+      }
+      for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * BATCH) {
+        uint64_t v[BATCH];
+#pragma unroll
+        for (int q = 0; q < BATCH; ++q) {
+          const uint32_t i = i0 + q * 32 + lane;
+          const uint64_t p = i < cnt ? P[pidx(i)] : row_offset;
+          const bool ok = p >= row_offset && p - row_offset < data.n;
+          if (i < cnt && !ok) atomicOr(err, err_bit(MS_E_RANGE));
+          const uint64_t r = ok ? p - row_offset : 0;
+          v[q] = !ok ? 0ull : (w == 64 ? __ldg(data.payload + r) : unpack_at(data.payload, r * w, w));
+        }
+#pragma unroll
+        for (int q = 0; q < BATCH; ++q) {
+          const uint32_t i = i0 + q * 32 + lane;
+          if (i < cnt) P[pidx(i)] = v[q];
+        }
+      }
     } else {
       for (uint32_t i = lane; i < cnt; i += 32) {
         const uint64_t p = P[pidx(i)];
