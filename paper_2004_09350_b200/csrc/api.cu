@@ -564,6 +564,12 @@ ms_status ms_decompress(const ms_ctx* ctx_, const ms_column* in, uint64_t* value
   uint32_t* err = sc.at<uint32_t>(o_meta);
   ColView src = view_of(in);
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+  if (in->fmt.format == MS_RLE) {  // runs expanded directly, no tile decode
+    MS_TRY_CUDA(launch_rle_expand(in->payload, src.run_starts, in->n_runs, in->n, values, ctx.s));
+    uint64_t h = 0;
+    MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), &h, 1));
+    return status_from_bits((uint32_t)h);
+  }
   ms_column o{};
   o.fmt = ms_fmt{MS_UNCOMPR, 0, 0, 0};
   o.n = in->n;

@@ -437,6 +437,43 @@ cudaError_t launch_chunk_run(const uint64_t* starts, uint64_t R, uint64_t n, uin
   return cudaGetLastError();
 }
 
+// RLE decompression (P:163 runs; S:115-131 decode): a warp takes 32 consecutive
+// runs, broadcasts each run's (value, start, end) by shuffle and writes its rows
+// with coalesced stores (lanes on consecutive rows): ~ceil(len/32) store
+// instructions per run, no per-row search or scan.
+__global__ void __launch_bounds__(256) rle_expand_kernel(const uint64_t* __restrict__ payload,
+                                                         const uint64_t* __restrict__ starts, uint64_t R, uint64_t n,
+                                                         uint64_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t k0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < R;
+       k0 += nwarps * 32) {
+    const uint64_t k = k0 + lane;
+    uint64_t v = 0, s = 0, e = 0;
+    if (k < R) {
+      v = __ldg(payload + 2 * k);
+      s = __ldg(starts + k);
+      e = min(__ldg(starts + k + 1), n);
+    }
+    const uint32_t nr = (uint32_t)min((uint64_t)32, R - k0);
+    for (uint32_t r = 0; r < nr; ++r) {
+      const uint64_t vr = __shfl_sync(kFull, v, r), sr = __shfl_sync(kFull, s, r), er = __shfl_sync(kFull, e, r);
+      for (uint64_t i = sr + lane; i < er; i += 32) out[i] = vr;
+    }
+  }
+}
+
+cudaError_t launch_rle_expand(const uint64_t* payload, const uint64_t* starts, uint64_t R, uint64_t n, uint64_t* out,
+                              cudaStream_t s) {
+  if (R == 0) return cudaSuccess;
+  uint64_t g = (R + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (g > cap) g = cap;
+  ProfScope prof_("rle_expand", s);
+  rle_expand_kernel<<<(int)g, 256, 0, s>>>(payload, starts, R, n, out);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------ RLE compression
 __global__ void __launch_bounds__(kThreads) rle_count_kernel(const uint64_t* __restrict__ v, uint64_t n,
                                                              uint32_t* counts) {

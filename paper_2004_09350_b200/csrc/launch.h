@@ -103,6 +103,8 @@ cudaError_t launch_rle2delta_pack(const ColView& c, uint32_t B, uint64_t nb, con
 // RLE run starts (exclusive prefix of lengths), validation against n
 cudaError_t launch_rle_starts(const uint64_t* payload, uint64_t R, uint64_t n, uint64_t* starts, uint64_t* status,
                               uint32_t* ticket, uint32_t* err, cudaStream_t s);
+cudaError_t launch_rle_expand(const uint64_t* payload, const uint64_t* starts, uint64_t R, uint64_t n, uint64_t* out,
+                              cudaStream_t s);
 cudaError_t launch_chunk_run(const uint64_t* starts, uint64_t R, uint64_t n, uint32_t* chunk_run, cudaStream_t s);
 // RLE compression of raw device values
 cudaError_t launch_rle_count(const uint64_t* v, uint64_t n, uint32_t* counts, cudaStream_t s);
