@@ -108,33 +108,45 @@ static uint64_t n_items_hint(const OutView& o) {
 }
 
 // ----------------------------------------------------------------- engine
+template <int F>
+static cudaError_t launch_staged(const ColView& src, const OutView& out, uint32_t* err, bool max_only,
+                                 cudaStream_t s) {
+  static bool attr[64][2] = {};  // per device and instantiation
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto k = max_only ? engine_staged_kernel<true, F> : engine_staged_kernel<false, F>;
+  const int dyn = (int)sizeof(StageSmem);
+  if (dev < 0 || dev >= 64 || !attr[dev][max_only]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr[dev][max_only] = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t items = n_items_hint(out);
+  uint64_t g = (uint64_t)per_sm * num_sms();
+  if (items < g) g = items;
+  StagedCol<F> sc{src, src.nb << src.log2B};
+  ProfScope prof_("engine_col", s);
+  k<<<(int)(g ? g : 1), kThreads, dyn, s>>>(sc, out, err);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s) {
   // staged input (stage.cuh) whenever tiles go in a static order: every output but
   // a block format written with the look-back
   const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP);
   static const bool unstaged = getenv("MS_ENGINE_UNSTAGED") != nullptr;
   if (stageable_format(src.format) && !out.n_dev && !ordered && !unstaged) {
-    static bool attr[64][2] = {};  // per device and instantiation
-    int dev = 0;
-    cudaGetDevice(&dev);
     const bool max_only = out.format == OUT_MAX_ONLY;
-    auto k = max_only ? engine_staged_kernel<true> : engine_staged_kernel<false>;
-    const int dyn = (int)sizeof(StageSmem);
-    if (dev < 0 || dev >= 64 || !attr[dev][max_only]) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-      if (e != cudaSuccess) return e;
-      if (dev >= 0 && dev < 64) attr[dev][max_only] = true;
+    switch (src.format) {
+      case MS_UNCOMPR: return launch_staged<MS_UNCOMPR>(src, out, err, max_only, s);
+      case MS_STATIC_BP: return launch_staged<MS_STATIC_BP>(src, out, err, max_only, s);
+      case MS_DYN_BP: return launch_staged<MS_DYN_BP>(src, out, err, max_only, s);
+      case MS_FOR_BP: return launch_staged<MS_FOR_BP>(src, out, err, max_only, s);
+      default: return launch_staged<MS_DELTA_BP>(src, out, err, max_only, s);
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t items = n_items_hint(out);
-    uint64_t g = (uint64_t)per_sm * num_sms();
-    if (items < g) g = items;
-    StagedCol sc{src, src.nb << src.log2B};
-    ProfScope prof_("engine_col", s);
-    k<<<(int)(g ? g : 1), kThreads, dyn, s>>>(sc, out, err);
-    return cudaGetLastError();
   }
   auto k = engine_kernel<ColSource>;
   int grid = persistent_grid(k, kThreads, n_items_hint(out));

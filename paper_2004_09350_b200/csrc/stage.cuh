@@ -44,12 +44,14 @@ __host__ __device__ inline bool stageable_format(int32_t f) {
   return f == MS_UNCOMPR || f == MS_STATIC_BP || f == MS_DYN_BP || f == MS_FOR_BP || f == MS_DELTA_BP;
 }
 
+// F: the source format (compile-time: no dead decode paths, fewer registers)
+template <int F>
 struct StagedCol {
   ColView c;
   uint64_t main_rows;  // block formats: nb * B
 
   __device__ __forceinline__ bool is_block() const {
-    return c.format == MS_DYN_BP || c.format == MS_FOR_BP || c.format == MS_DELTA_BP;
+    return F == MS_DYN_BP || F == MS_FOR_BP || F == MS_DELTA_BP;
   }
   // full blocks of tile t: [kb0, kb0 + nbk)
   __device__ __forceinline__ uint32_t tile_blocks(uint64_t t, uint64_t& kb0) const {
@@ -65,16 +67,16 @@ struct StagedCol {
     if (!nbk) return;
     const int tid = threadIdx.x;
     if (tid <= (int)nbk) st_cp4(&st.cw[slot][tid], c.cw + kb0 + tid);
-    if (c.format != MS_DYN_BP && tid < (int)nbk) st_cp8(&st.ref[slot][tid], c.ref + kb0 + tid);
+    if (F != MS_DYN_BP && tid < (int)nbk) st_cp8(&st.ref[slot][tid], c.ref + kb0 + tid);
   }
   // word range [lo, hi) of tile t's payload; block formats read it from the staged headers
   __device__ __forceinline__ void range(uint64_t t, uint32_t cnt, const StageSmem& st, int slot, uint64_t& lo,
                                         uint64_t& hi) const {
     const uint64_t r0 = t * kChunk;
-    if (c.format == MS_UNCOMPR) {
+    if (F == MS_UNCOMPR) {
       lo = r0;
       hi = r0 + cnt;
-    } else if (c.format == MS_STATIC_BP) {
+    } else if (F == MS_STATIC_BP) {
       lo = (r0 * c.w) >> 6;
       hi = ((r0 + cnt) * c.w + 63) >> 6;
     } else {
@@ -119,7 +121,7 @@ struct StagedCol {
       if (kMaxOnly) mx = v > mx ? v : mx;
       else sm.vals[i] = v;
     };
-    switch (c.format) {
+    switch (F) {
       case MS_UNCOMPR:
 #pragma unroll
         for (int q = 0; q < kVPT; ++q) {
@@ -159,7 +161,7 @@ struct StagedCol {
               if (sh + w > 64) x |= wd[wi + 1] << (64 - sh);
               x &= low_mask(w);
             }
-            put(i, c.format == MS_FOR_BP ? st.ref[slot][b] + x : x);
+            put(i, F == MS_FOR_BP ? st.ref[slot][b] + x : x);
           } else if (i < cnt) {
             put(i, __ldg(c.rem + (r0 + i - main_rows)));
           }
@@ -230,8 +232,8 @@ struct StagedCol {
 };
 
 // kMaxOnly: the auto-static-width pre-pass (OUT_MAX_ONLY), its own instantiation
-template <bool kMaxOnly>
-__global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol src, OutView out, uint32_t* err) {
+template <bool kMaxOnly, int F>
+__global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol<F> src, OutView out, uint32_t* err) {
   __shared__ EngineSmem sm;
   extern __shared__ __align__(16) unsigned char st_raw[];
   StageSmem& st = *reinterpret_cast<StageSmem*>(st_raw);
@@ -263,11 +265,11 @@ __global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol sr
     // an uncompressed source is encoded straight from its staging buffer (r0 is even:
     // no word offset)
     if (kMaxOnly) {  // auto static width: decode straight into a running max
-      src.decode<true>(t, cnt, st, buf, slot, sm, mx);
+      src.template decode<true>(t, cnt, st, buf, slot, sm, mx);
     } else {
       uint64_t* vals = sm.vals;
-      if (src.c.format == MS_UNCOMPR) vals = st.words[buf];
-      else src.decode<false>(t, cnt, st, buf, slot, sm, mx);
+      if (F == MS_UNCOMPR) vals = st.words[buf];
+      else src.template decode<false>(t, cnt, st, buf, slot, sm, mx);
       encode_tile(out, (uint32_t)t, r0, cnt, n, sm, err, vals);
     }
     __syncthreads();
