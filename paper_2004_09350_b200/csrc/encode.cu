@@ -89,10 +89,10 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
     if (r != cudaSuccess) return r;
     r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
     if (r != cudaSuccess) return r;
-    uint64_t cgrid = (n_full + 7) / 8;
+    uint64_t cgrid = (n_full + 31) / 32;  // 8 lanes per block
     if (cgrid > (uint64_t)env_int("MS_COPY_CTAS", 1 << 20)) cgrid = (uint64_t)env_int("MS_COPY_CTAS", 1 << 20);
     ProfScope prof_("pos_copy", s);
-    pos_copy_kernel<<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
+    pos_copy_kernel<8><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
     return cudaGetLastError();
   }
   if (n_full) {
@@ -221,10 +221,10 @@ cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64
   if (!block || !n_full) return cudaSuccess;
   r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
   if (r != cudaSuccess) return r;
-  uint64_t cgrid = (n_full + 7) / 8;
+  uint64_t cgrid = (n_full + 31) / 32;  // 8 lanes per block
   if (cgrid > (uint64_t)env_int("MS_COPY_CTAS", 1 << 20)) cgrid = (uint64_t)env_int("MS_COPY_CTAS", 1 << 20);
   ProfScope prof_("pos_copy", s);
-  pos_copy_kernel<<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
+  pos_copy_kernel<8><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
   return cudaGetLastError();
 }
 
@@ -266,7 +266,7 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
   uint64_t cgrid = (n_full + 7) / 8;
   if (cgrid > (uint64_t)env_int("MS_COPY_CTAS", 1 << 20)) cgrid = (uint64_t)env_int("MS_COPY_CTAS", 1 << 20);
   ProfScope prof_("project_copy", s);
-  pos_copy_kernel<<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
+  pos_copy_kernel<32><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
   return cudaGetLastError();
 }
 

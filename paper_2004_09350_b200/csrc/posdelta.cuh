@@ -425,24 +425,30 @@ __global__ void __launch_bounds__(kPdWarps * 32) pos_slot_kernel(const uint32_t*
   }
 }
 
-// one warp per block: slot -> payload at cw[k] * B / 64 (16-byte copies), cw[k+1]
+// LPB lanes per block (32 / LPB blocks per warp): slot -> payload at cw[k] * B / 64
+// (16-byte copies), cw[k+1]. Narrow blocks (positions, w ~ 5: 4w 16-byte units at
+// B = 512) take 8 lanes each, so a warp's header loads cover four blocks at once.
+template <int LPB>
 __global__ void __launch_bounds__(256) pos_copy_kernel(PosEnc e, uint64_t n_full, const uint64_t* __restrict__ slots,
                                                        uint32_t slot_words, const uint64_t* __restrict__ cwx,
                                                        uint32_t* err) {
-  const uint32_t lane = threadIdx.x & 31;
+  constexpr int kPerWarp = 32 / LPB;
+  const uint32_t lane = threadIdx.x & 31, sub = lane % LPB;
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t item = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < n_full;
-       item += nwarps) {
+  for (uint64_t w0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kPerWarp; w0 < n_full;
+       w0 += nwarps * kPerWarp) {
+    const uint64_t item = w0 + lane / LPB;
+    if (item >= n_full) continue;
     const uint64_t E = __ldg(cwx + item);
     const uint32_t w = (uint32_t)(__ldg(cwx + item + 1) - E);
-    if (lane == 0) {
+    if (sub == 0) {
       if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
       e.cw[item + 1] = (uint32_t)(E + w);
     }
     const uint32_t n2 = e.G / 128 * w;  // 16-byte units (B*w/64 words, B >= 128)
     const ulonglong2* src = reinterpret_cast<const ulonglong2*>(slots + item * slot_words);
     ulonglong2* dst = reinterpret_cast<ulonglong2*>(e.payload + E * (e.G / 64));
-    for (uint32_t m = lane; m < n2; m += 32) dst[m] = __ldg(src + m);
+    for (uint32_t m = sub; m < n2; m += LPB) dst[m] = __ldg(src + m);
   }
 }
 
