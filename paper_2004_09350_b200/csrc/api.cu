@@ -401,21 +401,22 @@ ms_status encode_into(const Ctx& ctx, Scratch& sc, uint64_t meta_off, uint64_t s
   if (fmt.format == MS_STATIC_BP) out->payload_words = cap;
   if (is_block(fmt.format)) MS_TRY_CUDA(cudaMemsetAsync(out->cw, 0, 4, ctx.s));  // cw[0] = 0 even when n = 0
   OutView ov = out_view(out, sc.at<uint64_t>(st_off), sc.at<uint32_t>(tk_off));
-  // block formats: slot mode (no look-back) when the tiles' slots (8 bytes per row) fit the budget
+  // block formats: slot mode (no look-back)
   const uint64_t n_tiles = (n + kChunk - 1) / kChunk, nb = is_block(fmt.format) ? n / fmt.block_size : 0;
-  const bool slot_mode = nb && n_tiles * kChunk * 8ull <= (8ull << 30) && !env_flag("MS_ENGINE_LOOKBACK");
+  // (8 bytes per row of slots; when they cannot be allocated the engine falls back
+  // to the in-order look-back, which needs no slots)
+  bool slot_mode = nb && !env_flag("MS_ENGINE_LOOKBACK");
   void* slot_mem = nullptr;
   uint64_t *cwx = nullptr, *scan_st = nullptr;
   uint32_t* scan_tk = nullptr;
+  const uint64_t chunks = (nb + kChunk - 1) / kChunk + 1;
   if (slot_mode) {
-    const uint64_t chunks = (nb + kChunk - 1) / kChunk + 1;
     const uint64_t bytes = align_up(n_tiles * kChunk * 8ull) + align_up(4 * nb) + align_up(8 * (nb + 2)) +
                            align_up(8 * chunks) + kAlign;
     slot_mem = ctx.alloc(bytes);
-    if (!slot_mem) {
-      release(ctx, out);
-      return MS_E_NOMEM;
-    }
+    slot_mode = slot_mem != nullptr;
+  }
+  if (slot_mode) {
     char* b = (char*)slot_mem;
     ov.slots = (uint64_t*)b;
     b += align_up(n_tiles * kChunk * 8ull);
