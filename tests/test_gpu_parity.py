@@ -100,6 +100,23 @@ def test_many_tiles_per_cta(kind, rng):
             assert_same_image(ms.morph(ga, b), O.morph(oa, *oracle_fmt(b)), f"morph {a}->{b} {kind} n={n}")
 
 
+@pytest.mark.parametrize("kind", ["sorted", "outlier", "wide"])
+def test_engine_lookback_fallback(kind, rng, monkeypatch):
+    """Block-format outputs through the in-order look-back engine (the fallback when
+    the per-tile slots cannot be allocated; forced by MS_ENGINE_LOOKBACK)."""
+    ms = get_ms()
+    monkeypatch.setenv("MS_ENGINE_LOOKBACK", "1")
+    n = (1 << 20) + 777
+    v = rand_values(n, kind, rng)
+    t = to_torch(v)
+    for f in (ms.dyn_bp(512), ms.for_bp(128), ms.delta_bp(2048)):
+        oc = O.encode(v, *oracle_fmt(f))
+        gc = ms.compress(t, f)
+        assert_same_image(gc, oc, f"lookback compress {f} {kind}")
+        for b in (ms.delta_bp(256), ms.dyn_bp(1024)):
+            assert_same_image(ms.morph(gc, b), O.morph(oc, *oracle_fmt(b)), f"lookback morph {f}->{b} {kind}")
+
+
 PREDS = None
 
 
