@@ -233,7 +233,7 @@ struct StagedCol {
 
 // kMaxOnly: the auto-static-width pre-pass (OUT_MAX_ONLY), its own instantiation
 template <bool kMaxOnly, int F>
-__global__ void __launch_bounds__(kThreads, 4) engine_staged_kernel(StagedCol<F> src, OutView out, uint32_t* err) {
+__global__ void __launch_bounds__(kThreads, 3) engine_staged_kernel(StagedCol<F> src, OutView out, uint32_t* err) {
   __shared__ EngineSmem sm;
   extern __shared__ __align__(16) unsigned char st_raw[];
   StageSmem& st = *reinterpret_cast<StageSmem*>(st_raw);
