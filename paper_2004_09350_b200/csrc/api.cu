@@ -381,7 +381,8 @@ ms_status encode_into(const Ctx& ctx, Scratch& sc, uint64_t meta_off, uint64_t s
                       uint64_t tk2_off, ms_fmt fmt, uint64_t n, uint64_t payload_cap_words, Launch launch,
                       ms_column* out) {
   uint32_t* err = sc.at<uint32_t>(meta_off);
-  if (fmt.format == MS_STATIC_BP && fmt.bit_width == 0) {  // auto width: max pass first
+  const bool auto_width = fmt.format == MS_STATIC_BP && fmt.bit_width == 0;
+  if (auto_width) {  // auto width: max pass first
     OutView mv{};
     mv.format = OUT_MAX_ONLY;
     mv.n = n;
@@ -401,6 +402,7 @@ ms_status encode_into(const Ctx& ctx, Scratch& sc, uint64_t meta_off, uint64_t s
   if (fmt.format == MS_STATIC_BP) out->payload_words = cap;
   if (is_block(fmt.format)) MS_TRY_CUDA(cudaMemsetAsync(out->cw, 0, 4, ctx.s));  // cw[0] = 0 even when n = 0
   OutView ov = out_view(out, sc.at<uint64_t>(st_off), sc.at<uint32_t>(tk_off));
+  ov.fits = auto_width;  // the width bounds every value by construction
   // block formats: slot mode (no look-back)
   const uint64_t n_tiles = (n + kChunk - 1) / kChunk, nb = is_block(fmt.format) ? n / fmt.block_size : 0;
   // (8 bytes per row of slots; when they cannot be allocated the engine falls back

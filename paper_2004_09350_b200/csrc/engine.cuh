@@ -27,6 +27,7 @@ struct OutView {
   uint64_t* status;          // look-back status, one per item
   uint32_t* ticket;
   unsigned long long* max_out;  // OUT_MAX_ONLY target
+  uint32_t fits;                // STATIC_BP: w came from the max pass, no value can overflow it
   // slot mode (block formats): tile k's blocks are packed into slots[k * kChunk ...]
   // (64 bits per row bounds every width), their widths go to bw[block]; the host
   // scans bw into cw and tile_copy_kernel moves every tile to its place — no look-back
@@ -97,7 +98,7 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
     }
     case MS_STATIC_BP: {
       const uint32_t w = o.w;
-      if (w < 64)
+      if (w < 64 && !o.fits)
         for (uint32_t i = tid; i < cnt; i += kThreads)
           if (vals[i] >> w) atomicOr(err, err_bit(MS_E_WIDTH_OVERFLOW));
       const uint64_t mask = low_mask(w);
