@@ -110,7 +110,26 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
         const uint32_t n32 = (cnt * w + 31) / 32, n32e = (n32 + 1) & ~1u;
         uint32_t* dst = reinterpret_cast<uint32_t*>(o.payload + wbase);
         const uint32_t m32 = 0xffffffffu >> (32 - w);
-        for (uint32_t m = tid; m < n32e; m += kThreads) dst[m] = m < n32 ? pack_word32(vals, cnt, w, m32, m, magic) : 0u;
+        const uint32_t* __restrict__ v32 = reinterpret_cast<const uint32_t*>(vals);
+        // word m's first code j = floor(32 m / w) at bit offset s = 32 m - j w; the
+        // thread's next word is kThreads words on = q codes + r bits (no division per word)
+        uint32_t j = div_small(32 * tid, w, magic), sb = 32 * tid - j * w;
+        const uint32_t q = (32 * kThreads) / w, r = 32 * kThreads - q * w;
+        for (uint32_t m = tid; m < n32e; m += kThreads) {
+          uint32_t acc = 0;
+          if (m < n32) {
+            acc = (v32[2 * j] & m32) >> sb;
+            uint32_t jj = j + 1, sh = w - sb;  // the next code starts at bit w - s of the word
+            for (; sh < 32 && jj < cnt; ++jj, sh += w) acc |= (v32[2 * jj] & m32) << sh;
+          }
+          dst[m] = acc;
+          j += q;
+          sb += r;
+          if (sb >= w) {
+            sb -= w;
+            ++j;
+          }
+        }
         return;
       }
       const uint64_t nwords = ((uint64_t)cnt * w + 63) / 64;
