@@ -827,6 +827,26 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
   if (out_fmt.format == MS_RLE) return MS_E_UNSUPPORTED;
   Ctx ctx(ctx_);
   const uint64_t n = positions->n;
+  // DELTA_BP / RLE data have no O(1) row access (D-12). When the positions are dense
+  // enough that the gather would decode most data tiles anyway (>= 1 per 64 rows),
+  // decode the column once (staged engine / rle_expand) and gather from its rows.
+  if ((data->fmt.format == MS_DELTA_BP || data->fmt.format == MS_RLE) && data->n && n * 64 >= data->n &&
+      8 * data->n <= (4ull << 30) && !env_flag("MS_PROJECT_NO_EXPAND")) {
+    uint64_t* tmp = (uint64_t*)ctx.alloc(8 * data->n);
+    if (tmp) {
+      ms_status st = ms_decompress(ctx_, data, tmp);
+      if (st == MS_OK) {
+        ms_column u{};
+        u.fmt = ms_fmt{MS_UNCOMPR, 0, 0, 0};
+        u.n = data->n;
+        u.payload_words = data->n;
+        u.payload = tmp;
+        st = ms_project(ctx_, &u, positions, row_offset, out_fmt, out);  // synchronises before returning
+      }
+      ctx.free(tmp);
+      return st;
+    }
+  }
   if (is_block(out_fmt.format) && 64 * (n / out_fmt.block_size) > 0xffffffffull) return MS_E_INVALID;
   const uint64_t items = (n + 127) / 128;  // enough for any item size (>= 128 rows)
   // the slot path (no look-back status) serves item sizes <= 512 into block formats or UNCOMPR

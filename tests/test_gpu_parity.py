@@ -192,6 +192,26 @@ def test_project(kind, rng):
                     assert_same_image(gr, orr, f"project {fd} @ {fp} -> {fo} {kind}")
 
 
+def test_project_sequential_data_gather(rng, monkeypatch):
+    """DELTA_BP / RLE data gathered tile by tile (the path for sparse positions; dense
+    positions decode the column first, which test_project covers)."""
+    ms = get_ms()
+    monkeypatch.setenv("MS_PROJECT_NO_EXPAND", "1")
+    n = 5 * 2048 + 13
+    v = rand_values(n, "sorted", rng)
+    t = to_torch(v)
+    pos = np.sort(rng.choice(n, 3000, replace=False)).astype(np.uint64)
+    for fd in (ms.delta_bp(128), ms.delta_bp(2048), ms.rle()):
+        gd = ms.compress(t, fd)
+        od = O.encode(v, *oracle_fmt(fd))
+        for fp in (ms.delta_bp(512), ms.uncompr()):
+            gp = ms.compress(to_torch(pos), fp)
+            op_ = O.encode(pos, *oracle_fmt(fp))
+            for fo in (ms.delta_bp(512), ms.uncompr(), ms.for_bp(128)):
+                assert_same_image(ms.project(gd, gp, 0, fo), O.project(od, op_, 0, *oracle_fmt(fo)),
+                                  f"project {fd} @ {fp} -> {fo} (tiled)")
+
+
 def test_project_range_error(rng):
     ms = get_ms()
     d = ms.compress(to_torch(np.arange(100, dtype=np.uint64)), ms.for_bp(128))
