@@ -241,10 +241,11 @@ __global__ void __launch_bounds__(kThreads) scan_reduce_kernel(In in, uint64_t N
   __shared__ uint64_t red[kThreads / 32];
   const uint64_t n_items = (N + kChunk - 1) / kChunk;
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const uint64_t base = item * kChunk + threadIdx.x * kVPT;
+    // the sum is order-free: lane-strided (coalesced) reads
+    const uint64_t base = item * kChunk + threadIdx.x;
     uint64_t t = 0;
 #pragma unroll
-    for (int q = 0; q < kVPT; ++q) t += base + q < N ? in(base + q) : 0;
+    for (int q = 0; q < kVPT; ++q) t += base + q * kThreads < N ? in(base + q * kThreads) : 0;
     t = warp_sum(t);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
     __syncthreads();
