@@ -123,7 +123,9 @@ typedef struct {
 typedef void *(*ms_alloc_fn)(void *alloc_ctx, size_t bytes, void *stream);
 typedef void (*ms_free_fn)(void *alloc_ctx, void *ptr, void *stream);
 
-#define MS_FLAG_SHRINK 1u /* copy variable-size outputs into an exact-size allocation */
+#define MS_FLAG_SHRINK 1u /* copy variable-size outputs into an exact-size allocation (default: a producer
+                           that sizes its output before the kernel keeps the slack of its provable capacity
+                           in alloc_bytes; nothing is copied) */
 
 typedef struct {
   void *stream;           /* cudaStream_t */
@@ -174,15 +176,19 @@ MS_API ms_status ms_project(const ms_ctx *ctx, const ms_column *data, const ms_c
  * D-13), or, with positions != NULL, of data[pos - row_offset] over positions
  * (select -> project -> sum fused). Uses the format identities where
  * they apply: RLE sum v*len, FOR B*ref + sum codes, DELTA
- * B*base + sum (B-j)*d_j. Never synchronises; *sum is overwritten. */
+ * B*base + sum (B-j)*d_j. Never synchronises; *sum is overwritten.
+ * Host-side validation errors are returned; device-side errors (MS_E_RANGE for
+ * a position outside [row_offset, row_offset + in->n), MS_E_CORRUPT for a
+ * corrupt RLE body or width table) are ORed into the library's sticky device
+ * error word and reported ONLY by ms_check_errors (no other call reads it). */
 MS_API ms_status ms_agg_sum(const ms_ctx *ctx, const ms_column *in, const ms_column *positions, uint64_t row_offset,
                      uint64_t *sum);
 
 /* agg_sum_grouped: sums[g] = sum of vals_i with gid_i = g, g < n_groups, mod 2^64;
  * output uncompressed. sums: device, n_groups uint64,
  * overwritten. MS_E_INVALID if gid->n != vals->n (LengthMismatch S:316);
- * MS_E_RANGE if a gid >= n_groups (reported at the next synchronising call or
- * by ms_check_errors). Never synchronises. */
+ * MS_E_RANGE if a gid >= n_groups (a device-side error: reported only by
+ * ms_check_errors, like ms_agg_sum's). Never synchronises. */
 MS_API ms_status ms_agg_sum_grouped(const ms_ctx *ctx, const ms_column *gid, const ms_column *vals, uint64_t n_groups,
                              uint64_t *sums);
 
@@ -192,7 +198,10 @@ MS_API ms_status ms_agg_sum_grouped(const ms_ctx *ctx, const ms_column *gid, con
  * device column. ms_column_to_host: copies the device column's sections into
  * caller-owned HOST buffers given in host_col (pointers must be sized for the
  * device column's sections; descriptor fields are filled in). Both enqueue on
- * ctx->stream; ms_column_to_host synchronises. */
+ * ctx->stream; ms_column_to_host synchronises. ms_column_to_device validates a
+ * block-format image on the host before any allocation or copy: cw[0] = 0, cw
+ * non-decreasing, every block width <= 64 and payload_words = cw[nb] * B / 64,
+ * else MS_E_CORRUPT. */
 MS_API ms_status ms_column_to_device(const ms_ctx *ctx, const ms_column *host_col, ms_column *out);
 MS_API ms_status ms_column_to_host(const ms_ctx *ctx, const ms_column *dev_col, ms_column *host_col);
 

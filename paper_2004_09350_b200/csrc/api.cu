@@ -262,23 +262,37 @@ OutView out_view(ms_column* o, uint64_t* status, uint32_t* ticket) {
   return v;
 }
 
+// device-to-device copy of the four image sections of `in` into `out` (same shape)
+cudaError_t copy_sections(const Ctx& ctx, const ms_column* in, ms_column* out) {
+  cudaError_t e = cudaSuccess;
+  if (in->payload_words)
+    e = cudaMemcpyAsync(out->payload, in->payload, 8 * in->payload_words, cudaMemcpyDeviceToDevice, ctx.s);
+  if (e == cudaSuccess && is_block(in->fmt.format)) {
+    e = cudaMemcpyAsync(out->cw, in->cw, 4 * (in->n_blocks + 1), cudaMemcpyDeviceToDevice, ctx.s);
+    if (e == cudaSuccess && out->ref && in->n_blocks)
+      e = cudaMemcpyAsync(out->ref, in->ref, 8 * in->n_blocks, cudaMemcpyDeviceToDevice, ctx.s);
+    if (e == cudaSuccess && in->n_rem)
+      e = cudaMemcpyAsync(out->rem, in->rem, 8 * in->n_rem, cudaMemcpyDeviceToDevice, ctx.s);
+  }
+  return e;
+}
+
 // Copy a column whose payload was over-allocated into an exact-size allocation
-// when asked to (MS_FLAG_SHRINK) or when more than 1 GiB would be wasted.
+// when asked to (MS_FLAG_SHRINK); otherwise the slack stays with the column (no copy).
 ms_status maybe_shrink(const Ctx& ctx, ms_column* out) {
   const uint64_t need = align_up(8 * out->payload_words);
   const uint64_t have = (uint64_t)((char*)(out->cw ? (void*)out->cw : (void*)nullptr) - (char*)out->payload);
   const bool force = ctx.c && (ctx.c->flags & MS_FLAG_SHRINK);
-  if (!out->cw || have <= need) return MS_OK;
-  if (!force && have - need < (1ull << 30)) return MS_OK;
+  if (!out->cw || have <= need || !force) return MS_OK;
   ms_column t;
   MS_TRY(alloc_column(ctx, &t, out->fmt, out->n, out->payload_words, out->n_runs));
   t.payload_words = out->payload_words;
   t.fmt.max_width = out->fmt.max_width;
-  MS_TRY_CUDA(cudaMemcpyAsync(t.payload, out->payload, 8 * out->payload_words, cudaMemcpyDeviceToDevice, ctx.s));
-  MS_TRY_CUDA(cudaMemcpyAsync(t.cw, out->cw, 4 * (out->n_blocks + 1), cudaMemcpyDeviceToDevice, ctx.s));
-  if (out->ref && out->n_blocks)
-    MS_TRY_CUDA(cudaMemcpyAsync(t.ref, out->ref, 8 * out->n_blocks, cudaMemcpyDeviceToDevice, ctx.s));
-  if (out->n_rem) MS_TRY_CUDA(cudaMemcpyAsync(t.rem, out->rem, 8 * out->n_rem, cudaMemcpyDeviceToDevice, ctx.s));
+  const cudaError_t e = copy_sections(ctx, out, &t);
+  if (e != cudaSuccess) {
+    release(ctx, &t);  // the caller releases *out on error
+    return cuda_status(e);
+  }
   release(ctx, out);
   *out = t;
   return MS_OK;
@@ -486,6 +500,51 @@ ms_status compress_rle(const Ctx& ctx, const uint64_t* values, uint64_t n, ms_co
   return MS_OK;
 }
 
+// select -> DELTA_BP{512} in one pass (select_pos.cu): the output is allocated at
+// a provable capacity before the kernel (select_pos_width_bound; the kernel writes
+// every block at its final place) and described exactly after the op's single
+// read-back. The allocation keeps its slack (no copy) unless MS_FLAG_SHRINK is set.
+ms_status select_positions_onepass(const Ctx& ctx, const ms_column* in, const PredSpec& ps, uint64_t row_offset,
+                                   const ms_fmt& f, ms_column* out) {
+  const uint64_t n = in->n;
+  const uint32_t B = f.block_size;
+  const uint64_t T = select_pos_tiles(n);
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_tk = sc.add(8, true);
+  const uint64_t o_st1 = sc.add(8 * T, true);
+  const uint64_t o_st2 = sc.add(8 * T, true);
+  const uint64_t o_cnt = sc.add(4 * T, false);
+  const uint64_t o_tail = sc.add(2 * (uint64_t)(B - 1) * T, false);
+  if (!sc.commit()) return MS_E_NOMEM;
+  const uint64_t nbmax = n / B;
+  uint64_t wsum = select_pos_width_bound(n, B);
+  if (wsum > 64 * nbmax) wsum = 64 * nbmax;
+  const uint64_t cap = wsum * (B / 64);
+  MS_TRY(alloc_column(ctx, out, f, nbmax * B + (B - 1), cap, 0));
+  uint64_t* meta = sc.at<uint64_t>(o_meta);
+  cudaError_t e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
+  if (e == cudaSuccess)
+    e = launch_select_pos(view_of(in), ps, B, row_offset, sc.at<uint32_t>(o_tk), sc.at<uint64_t>(o_st1),
+                          sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_cnt), sc.at<uint16_t>(o_tail), meta,
+                          reinterpret_cast<uint32_t*>(meta), out->payload, out->cw, out->ref, out->rem, cap, ctx.s);
+  uint64_t h[4] = {0, 0, 0, 0};
+  ms_status st = e == cudaSuccess ? readback(ctx, meta, h, 4) : cuda_status(e);  // the op's one sync
+  if (st == MS_OK) st = status_from_bits((uint32_t)h[0]);
+  if (st != MS_OK) {
+    release(ctx, out);
+    return st;
+  }
+  out->n = h[1];
+  out->n_blocks = h[1] / B;
+  out->n_rem = h[1] % B;
+  out->payload_words = h[2] * (B / 64);
+  out->fmt.max_width = (uint32_t)h[3];
+  if (ctx.c && (ctx.c->flags & MS_FLAG_SHRINK)) st = maybe_shrink(ctx, out);
+  if (st != MS_OK) release(ctx, out);
+  return st;
+}
+
 // worst-case payload words of a block-format column of n values when every
 // block may need 64 bits
 uint64_t full_cap(uint64_t n, uint32_t B) { return (n / B) * B; }
@@ -596,14 +655,10 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
     MS_TRY(alloc_column(ctx, out, in->fmt, n, in->payload_words, in->n_runs));
     out->payload_words = in->payload_words;
     out->fmt.max_width = in->fmt.max_width;
-    if (in->payload_words)
-      MS_TRY_CUDA(cudaMemcpyAsync(out->payload, in->payload, 8 * in->payload_words, cudaMemcpyDeviceToDevice, ctx.s));
-    if (is_block(fmt.format)) {
-      MS_TRY_CUDA(cudaMemcpyAsync(out->cw, in->cw, 4 * (in->n_blocks + 1), cudaMemcpyDeviceToDevice, ctx.s));
-      if (out->ref && in->n_blocks)
-        MS_TRY_CUDA(cudaMemcpyAsync(out->ref, in->ref, 8 * in->n_blocks, cudaMemcpyDeviceToDevice, ctx.s));
-      if (in->n_rem)
-        MS_TRY_CUDA(cudaMemcpyAsync(out->rem, in->rem, 8 * in->n_rem, cudaMemcpyDeviceToDevice, ctx.s));
+    const cudaError_t e = copy_sections(ctx, in, out);
+    if (e != cudaSuccess) {
+      release(ctx, out);  // *out zeroed, nothing leaks
+      return cuda_status(e);
     }
     return MS_OK;
   }
@@ -690,6 +745,8 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   MS_TRY(make_pred(pred, ps));
   Ctx ctx(ctx_);
   const uint64_t n = in->n;
+  if (out_fmt.format == MS_DELTA_BP && select_pos_supported(view_of(in), out_fmt.block_size))
+    return select_positions_onepass(ctx, in, ps, row_offset, out_fmt, out);
   const uint64_t NS = (n + kSegRows - 1) / kSegRows;  // 512-row segments
   const uint64_t n_words = NS * kSegWords;
   const uint32_t G = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;  // output item size
@@ -1001,16 +1058,20 @@ ms_status ms_column_to_device(const ms_ctx* ctx_, const ms_column* h, ms_column*
   std::memset(out, 0, sizeof(*out));
   MS_TRY(check_col(h));
   Ctx ctx(ctx_);
-  MS_TRY(alloc_column(ctx, out, h->fmt, h->n, h->payload_words, h->n_runs));
-  out->payload_words = h->payload_words;
-  if (is_block(h->fmt.format)) {  // the max_width hint, from the host copy of cw
-    uint32_t mw = 0;
+  uint32_t mw = 0;
+  if (is_block(h->fmt.format)) {  // validate the host width table; the max_width hint
+    if (h->cw[0] != 0) return MS_E_CORRUPT;
     for (uint64_t b = 0; b < h->n_blocks; ++b) {
+      if (h->cw[b + 1] < h->cw[b]) return MS_E_CORRUPT;
       const uint32_t w = h->cw[b + 1] - h->cw[b];
+      if (w > 64) return MS_E_CORRUPT;
       mw = w > mw ? w : mw;
     }
-    out->fmt.max_width = mw <= 64 ? mw : 0;
+    if ((uint64_t)h->cw[h->n_blocks] * (h->fmt.block_size / 64) != h->payload_words) return MS_E_CORRUPT;
   }
+  MS_TRY(alloc_column(ctx, out, h->fmt, h->n, h->payload_words, h->n_runs));
+  out->payload_words = h->payload_words;
+  if (is_block(h->fmt.format)) out->fmt.max_width = mw;
   auto cp = [&](void* d, const void* s, uint64_t bytes) {
     return bytes ? cudaMemcpyAsync(d, s, bytes, cudaMemcpyHostToDevice, ctx.s) : cudaSuccess;
   };

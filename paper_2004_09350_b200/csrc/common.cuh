@@ -417,7 +417,7 @@ __device__ __forceinline__ void load_rows(const ColView& c, uint64_t r0, uint32_
         if (k >= c.nruns) break;
         const uint64_t s = __ldg(c.run_starts + k);
         if (s >= r0 + cnt) break;
-        sm.vals[s - r0] = 1;
+        if (s > r0) sm.vals[s - r0] = 1;  // s <= r0: corrupt (non-monotone) starts, reported by StartsEpi
       }
       __syncthreads();
       uint64_t loc[kVPT];

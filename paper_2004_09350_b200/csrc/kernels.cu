@@ -421,7 +421,9 @@ struct StartsEpi : NoKey {
   uint32_t* err;
   __device__ void operator()(uint64_t idx, uint64_t off, uint64_t len) const {
     starts[idx] = off;
-    if (len == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+    // every length is >= 1 and every run ends inside the column: this also catches
+    // totals that wrap mod 2^64 (non-monotone starts)
+    if (len == 0 || len > n || off > n - len) atomicOr(err, err_bit(MS_E_CORRUPT));
   }
   __device__ void total(uint64_t t) const {
     starts[R] = t;

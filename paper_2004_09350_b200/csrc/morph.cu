@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(256) rle2delta_width_kernel(ColView c, uint32_
   const uint64_t main_rows = nb << log2B;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < c.nruns; k += stride) {
     const uint64_t v = __ldg(c.payload + 2 * k);
-    const uint64_t s = __ldg(c.run_starts + k), e = __ldg(c.run_starts + k + 1);  // rows [s, e)
+    // rows [s, e), clamped to the column (a corrupt body is reported by StartsEpi)
+    const uint64_t s = __ldg(c.run_starts + k), e = min(__ldg(c.run_starts + k + 1), c.n);
     if (s >= e) continue;
     if (k > 0 && s < main_rows && (s & (B - 1))) {
       const uint64_t d = v - __ldg(c.payload + 2 * (k - 1));
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) rle2delta_pack_kernel(ColView c, uint32_t
   const uint64_t main_rows = nb << log2B;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < c.nruns; k += stride) {
     const uint64_t s = __ldg(c.run_starts + k);
-    if (k == 0 || s >= main_rows || !(s & (B - 1)) || s >= __ldg(c.run_starts + k + 1)) continue;
+    if (k == 0 || s >= main_rows || !(s & (B - 1)) || s >= min(__ldg(c.run_starts + k + 1), c.n)) continue;
     const uint64_t b = s >> log2B;
     const uint64_t d = __ldg(c.payload + 2 * k) - __ldg(c.payload + 2 * (k - 1));
     const uint64_t c0 = cwx[b];

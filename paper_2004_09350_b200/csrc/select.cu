@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(256) rle_mask_kernel(ColView c, Pred pred, uin
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < c.nruns; k += stride) {
     if (!pred(__ldg(c.payload + 2 * k))) continue;
-    const uint64_t a = __ldg(c.run_starts + k), e = __ldg(c.run_starts + k + 1);  // rows [a, e)
+    // rows [a, e), clamped to the column: a corrupt body (reported by StartsEpi)
+    // never writes outside the mask
+    const uint64_t a = __ldg(c.run_starts + k), e = min(__ldg(c.run_starts + k + 1), c.n);
     if (a >= e) continue;
     const uint64_t wa = a >> 5, we = (e - 1) >> 5;
     const uint32_t ma = ~0u << (a & 31), me = ~0u >> (31 - ((e - 1) & 31));

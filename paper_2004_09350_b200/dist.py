@@ -30,9 +30,9 @@ def allgather_counts(count: int, device) -> list[int]:
     """C1: every rank's selected count (one int64 per rank)."""
     world = dist.get_world_size()
     t = torch.tensor([count], dtype=torch.int64, device=device)
-    out = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(out, t)
-    return [int(x.item()) for x in out]
+    out = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, t)
+    return out.tolist()  # one device -> host read for all ranks
 
 
 def exclusive_offsets(counts: list[int]) -> list[int]:

@@ -184,16 +184,32 @@ def _ptr(t) -> int:
 
 
 class Column:
-    """A device column owned by Python (released through ms_column_release)."""
+    """A device column owned by Python (released through ms_column_release).
 
-    def __init__(self, c: _Column, owned: bool = True):
+    The column's allocation belongs to the stream it was created on (PyTorch's
+    caching allocator reuses a freed block in that stream's order). Every op
+    records the other streams that read the column; on release the creating
+    stream first waits for an event recorded on each of them, so the memory is
+    not handed out again while their kernels may still read it."""
+
+    def __init__(self, c: _Column, owned: bool = True, stream: Optional[torch.cuda.Stream] = None):
         self._c = c
         self._owned = owned
+        self._stream = stream if stream is not None else torch.cuda.current_stream()
+        self._users = {}
+
+    def _used_on(self, stream: torch.cuda.Stream):
+        if stream.cuda_stream != self._stream.cuda_stream:
+            self._users[stream.cuda_stream] = stream
 
     def __del__(self):
         try:
             if self._owned and self._c.alloc:
-                _lib.ms_column_release(ctypes.byref(_ctx()), ctypes.byref(self._c))
+                for s in self._users.values():
+                    ev = torch.cuda.Event()
+                    ev.record(s)
+                    self._stream.wait_event(ev)
+                _lib.ms_column_release(ctypes.byref(_ctx(self._stream)), ctypes.byref(self._c))
         except Exception:
             pass
 
@@ -262,6 +278,19 @@ class Column:
         return f"Column({self.fmt}, n={self.n}, bytes={self.footprint()})"
 
 
+def _stream_of(stream) -> torch.cuda.Stream:
+    return stream if stream is not None else torch.cuda.current_stream()
+
+
+def _uses(stream, *cols):
+    """Record that an op on `stream` reads `cols` (see Column)."""
+    s = _stream_of(stream)
+    for c in cols:
+        if c is not None:
+            c._used_on(s)
+    return s
+
+
 def _fmt(f) -> _Fmt:
     f = Fmt(*f) if not isinstance(f, Fmt) else f
     return _Fmt(f.format, f.bit_width, f.block_size, 0)
@@ -274,13 +303,14 @@ def compress(values, fmt, n: Optional[int] = None, stream=None, flags: int = 0) 
     out = _Column()
     _check(_lib.ms_compress(ctypes.byref(_ctx(stream, flags)), _ptr(values) if n else None, n, _fmt(fmt),
                             ctypes.byref(out)), "ms_compress")
-    return Column(out)
+    return Column(out, stream=_stream_of(stream))
 
 
 def decompress(col: Column, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """ms_decompress into a torch.int64 CUDA tensor (uint64 bit patterns)."""
     if out is None:
         out = torch.empty(col.n, dtype=torch.int64, device="cuda")
+    _uses(stream, col)
     _check(_lib.ms_decompress(ctypes.byref(_ctx(stream)), ctypes.byref(col._c), _ptr(out) if col.n else None),
            "ms_decompress")
     return out
@@ -288,9 +318,10 @@ def decompress(col: Column, out: Optional[torch.Tensor] = None, stream=None) -> 
 
 def morph(col: Column, fmt, stream=None, flags: int = 0) -> Column:
     out = _Column()
+    s = _uses(stream, col)
     _check(_lib.ms_morph(ctypes.byref(_ctx(stream, flags)), ctypes.byref(col._c), _fmt(fmt), ctypes.byref(out)),
            "ms_morph")
-    return Column(out)
+    return Column(out, stream=s)
 
 
 def select(col: Column, op: int, a: int = 0, b: int = 0, bitmap: Optional[torch.Tensor] = None,
@@ -300,9 +331,10 @@ def select(col: Column, op: int, a: int = 0, b: int = 0, bitmap: Optional[torch.
     p = _Pred(op=op, a=a & (2**64 - 1), b=b & (2**64 - 1), bitmap=_ptr(bitmap) if bitmap is not None else None,
               bitmap_bits=bitmap_bits)
     out = _Column()
+    s = _uses(stream, col)
     _check(_lib.ms_select(ctypes.byref(_ctx(stream, flags)), ctypes.byref(col._c), ctypes.byref(p), row_offset,
                           _fmt(out_fmt), ctypes.byref(out)), "ms_select")
-    return Column(out)
+    return Column(out, stream=s)
 
 
 def project(data: Column, positions: Column, row_offset: int = 0, out_fmt=None, stream=None,
@@ -310,28 +342,38 @@ def project(data: Column, positions: Column, row_offset: int = 0, out_fmt=None, 
     if out_fmt is None:
         out_fmt = uncompr()
     out = _Column()
+    s = _uses(stream, data, positions)
     _check(_lib.ms_project(ctypes.byref(_ctx(stream, flags)), ctypes.byref(data._c), ctypes.byref(positions._c),
                            row_offset, _fmt(out_fmt), ctypes.byref(out)), "ms_project")
-    return Column(out)
+    return Column(out, stream=s)
 
 
 def agg_sum(col: Column, positions: Optional[Column] = None, row_offset: int = 0,
-            out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """ms_agg_sum -> 1-element torch.int64 CUDA tensor holding the uint64 sum bits (no sync)."""
+            out: Optional[torch.Tensor] = None, stream=None, check: bool = False) -> torch.Tensor:
+    """ms_agg_sum -> 1-element torch.int64 CUDA tensor holding the uint64 sum bits
+    (no sync). Device-side errors (a position out of range, a corrupt body) reach
+    only the sticky error word: check=True reads it (ms_check_errors, one sync)."""
     if out is None:
         out = torch.empty(1, dtype=torch.int64, device="cuda")
+    _uses(stream, col, positions)
     _check(_lib.ms_agg_sum(ctypes.byref(_ctx(stream)), ctypes.byref(col._c),
                            ctypes.byref(positions._c) if positions is not None else None, row_offset, _ptr(out)),
            "ms_agg_sum")
+    if check:
+        check_errors(stream)
     return out
 
 
 def agg_sum_grouped(gid: Column, vals: Column, n_groups: int, out: Optional[torch.Tensor] = None,
-                    stream=None) -> torch.Tensor:
+                    stream=None, check: bool = False) -> torch.Tensor:
+    """ms_agg_sum_grouped (no sync); check=True reads the sticky error word (MS_E_RANGE for a gid >= n_groups)."""
     if out is None:
         out = torch.empty(n_groups, dtype=torch.int64, device="cuda")
+    _uses(stream, gid, vals)
     _check(_lib.ms_agg_sum_grouped(ctypes.byref(_ctx(stream)), ctypes.byref(gid._c), ctypes.byref(vals._c),
                                    n_groups, _ptr(out) if n_groups else None), "ms_agg_sum_grouped")
+    if check:
+        check_errors(stream)
     return out
 
 

@@ -90,6 +90,10 @@ def test_c2_full():
     X, Y, pos, yp, yu = c2_chain(ms, a["n"])
     assert pos.n == a["count"]
     assert ms.u64(ms.agg_sum(yp)) == ms.u64(ms.agg_sum(yu)) == a["sum_projected"]
+    # full-size image anchors (oracle-computed: 1,476,652 / 2,624,044 B)
+    assert pos.footprint() == a["positions_bytes"]
+    assert yp.footprint() == a["yp_for_bytes"]
+    assert yu.footprint() == a["yp_uncompr_bytes"]
     check_sampled_positions(ms, pos, lambda m, s: synth.gen_host("c2.X", m, s), O.EQ, 17,
                             samples=((0, 1 << 20), (a["n"] - (1 << 20), a["n"])))
 
@@ -143,19 +147,44 @@ def test_c3_full():
     assert int(p[0]) == a["first"] and int(p[-1]) == a["last"]
     assert ms.u64(ms.agg_sum(R, pr)) == ms.u64(ms.agg_sum(D, pd)) == a["sum_selected"]
     m1 = ms.morph(R, ms.delta_bp(2048))
-    assert_same_image(m1, _images_of(ms, D), "c3 morph RLE -> DELTA_BP{2048} == compress")
+    check_sampled_delta_blocks(m1, a["n"], 2048, "c3 morph RLE -> DELTA_BP{2048}")
+    assert 8 * m1.payload_words == a["delta_bp2048_payload_bytes"]
     m2 = ms.morph(D, ms.static_bp(0))
     assert m2.fmt.bit_width == a["static_bp_auto_width"]
-    assert ms.u64(ms.agg_sum(m2)) == ms.u64(ms.agg_sum(D))
+    check_sampled_static_rows(m2, a["n"], "c3 morph DELTA_BP{2048} -> STATIC_BP{auto}")
+    assert ms.u64(ms.agg_sum(m2)) == ms.u64(ms.agg_sum(D)) == a["sum_all"]
 
 
-def _images_of(ms, col):
-    """A GPU column's images in the oracle's OColumn shape (GPU vs GPU check)."""
+SAMPLE_BLOCKS = (0, 1, 777, 65_536, 131_071, 200_003, 262_143)
+
+
+def check_sampled_delta_blocks(col, n, B, what):
+    """Full-size DELTA_BP column vs the oracle, block by block: blocks are
+    independent (D-6), so block b's payload words, cw step and base equal the
+    oracle's image of rows [bB, bB + B) alone (c3 rows from the host generator)."""
     img = col.images()
-    f = col.fmt
-    return O.OColumn(format=int(f.format), bit_width=f.bit_width, block_size=f.block_size, n=col.n,
-                     n_blocks=col.n_blocks, n_rem=col.n_rem, n_runs=col.n_runs, payload=img["payload"],
-                     cw=img["cw"], ref=img["ref"], rem=img["rem"])
+    for b in SAMPLE_BLOCKS:
+        if b >= n // B:
+            continue
+        oc = O.encode(synth.gen_host("c3.x", B, b * B), O.DELTA_BP, 0, B)
+        w0, w1 = int(img["cw"][b]), int(img["cw"][b + 1])
+        assert w1 - w0 == int(oc.cw[1]), (what, b)
+        assert int(img["ref"][b]) == int(oc.ref[0]), (what, b)
+        got = img["payload"][w0 * (B // 64):w1 * (B // 64)]
+        assert np.array_equal(got, oc.payload), (what, b)
+
+
+def check_sampled_static_rows(col, n, what):
+    """Full-size STATIC_BP{w} column vs the oracle on sampled 64-row groups: rows
+    [r0, r0 + 64) with 64 | r0 occupy exactly words [r0 w / 64, (r0 + 64) w / 64)."""
+    w = col.fmt.bit_width
+    pay = col.images()["payload"]
+    for b in SAMPLE_BLOCKS:
+        r0 = (b * 2048 + 64 * (b % 29)) % (n - 64)
+        r0 -= r0 % 64
+        oc = O.encode(synth.gen_host("c3.x", 64, r0), O.STATIC_BP, w)
+        got = pay[r0 * w // 64:(r0 + 64) * w // 64]
+        assert np.array_equal(got, oc.payload), (what, r0)
 
 
 # ------------------------------------------------------------------ c4 (D-16 chain)
@@ -214,6 +243,9 @@ def test_c4_full():
     g = c4_chain(ms, a["n"])
     assert g["pos1"].n == a["count_pos1"]
     assert g["pos2"].n == a["count_pos2"]
+    # full-size image anchors (oracle-computed; 66,462,044 / 4,719,624 B)
+    assert g["pos1"].footprint() == a["pos1_bytes"]
+    assert g["pos2"].footprint() == a["pos2_bytes"]
     assert ms.u64(ms.agg_sum(g["m1p"])) == a["sum_m1"]
     assert ms.u64(ms.agg_sum(g["m2p"])) == a["sum_m2"]
     assert [int(x) for x in g["g1"]] == a["grouped_m1"]
@@ -258,6 +290,41 @@ def test_c5_full():
     assert pos.n == a["count"]
     yp = ms.project(Y, pos, 0, ms.for_bp(512))
     assert ms.u64(ms.agg_sum(yp)) == a["sum_projected"]
+    # full-size image anchors (oracle-computed; 245,585,644 / 677,386,156 B)
+    assert pos.footprint() == a["positions_bytes"]
+    assert yp.footprint() == a["yp_bytes"]
     del Y, yp
     check_sampled_positions(ms, pos, lambda m, s: synth.gen_host("c5.X", m, s), O.LT, 1 << 16,
                             samples=((0, 1 << 20), (n // 2, n // 2 + (1 << 20)), (n - (1 << 20), n)))
+
+
+def test_c5_eight_shards_full():
+    """BJ.c5's G = 8 layout emulated on one GPU, shard after shard (D-18, SURVEY.md
+    §8(e)): each 2^29-row shard's count equals the oracle's per-shard count, each
+    shard's positions / Y' image sizes equal the oracle's images of that shard,
+    the C1 offsets are the exclusive scan of the counts, and the shard sums add
+    up (mod 2^64) to the single-column sum."""
+    ms = get_ms()
+    from paper_2004_09350_b200 import dist as D
+    a = anchors()["c5"]
+    n, G = a["n"], 8
+    counts, total = [], 0
+    for s in range(G):
+        start, end = D.shard_range(n, G, s)
+        m = end - start
+        X = ms.compress(dev("c5.X", m, start), ms.dyn_bp(512))
+        Y = ms.compress(dev("c5.Y", m, start), ms.for_bp(512))
+        pos = ms.select(X, ms.LT, 1 << 16, row_offset=start, out_fmt=ms.delta_bp(512))
+        yp = ms.project(Y, pos, start, ms.for_bp(512))
+        counts.append(pos.n)
+        assert pos.footprint() == a["positions_bytes_g8"][s], s
+        assert yp.footprint() == a["yp_bytes_g8"][s], s
+        total += ms.u64(ms.agg_sum(yp))
+        if s == 0:  # the shard's first positions are global row ids of shard 0
+            check_sampled_positions(ms, pos, lambda mm, ss: synth.gen_host("c5.X", mm, ss), O.LT, 1 << 16,
+                                    samples=((0, 1 << 18),))
+        del X, Y, pos, yp
+    assert counts == a["shard_counts_g8"]
+    offs = D.exclusive_offsets(counts)
+    assert offs[0] == 0 and offs[1] == a["shard_counts_g8"][0] and offs[-1] + counts[-1] == a["count"]
+    assert total % (1 << 64) == a["sum_projected"]

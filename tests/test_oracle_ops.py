@@ -179,3 +179,19 @@ def test_morph_all_pairs(kind):
         same = O.morph(ca, *a)  # identity morph is byte-identical
         for s in ("payload", "cw", "ref", "rem"):
             assert np.array_equal(getattr(same, s), getattr(ca, s))
+
+
+@pytest.mark.parametrize("op", [O.EQ, O.NE, O.LT, O.LE, O.GT, O.GE, O.BETWEEN, O.IN_BITMAP])
+def test_count_raw_brute_force(op):
+    """orc_count_raw (the predicate count on a raw vector, D-11 / S:271)
+    against numpy's own comparison operators, including the saturating
+    constants 0 and 2^64-1 and an empty range."""
+    v = np.concatenate([RNG.integers(0, 1 << 12, 3000, dtype=np.uint64),
+                        np.array([0, 1, M64, M64 - 1, 4095, 4096], np.uint64)])
+    bm = RNG.integers(0, 1 << 63, 70, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    cases = [(0, 0), (1, 4095), (2000, 2100), (M64, 0), (M64 - 1, M64), (2100, 2000)]
+    for a, b in cases:
+        bits = 4000 if op == O.IN_BITMAP else 0
+        want = int(np_pred(v, op, a, b, bm, bits).sum())
+        got = O.count_raw(v, op, a, b, bitmap=bm if op == O.IN_BITMAP else None, bitmap_bits=bits)
+        assert got == want, (op, a, b)

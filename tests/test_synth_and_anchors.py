@@ -51,3 +51,24 @@ def test_c1_anchors():
     assert (np.count_nonzero(w == 6), np.count_nonzero(w == 7)) == (107, 96)
     assert O.agg_sum(xc, pos) == 5_277_336
     assert O.agg_sum(O.project(xc, pos, 0, O.UNCOMPR)) == 5_277_336
+
+
+def test_full_size_anchor_file_matches_survey():
+    """tests/golden/config_anchors.json is written by tools/make_anchors.py from
+    oracle/ only; its image sizes must equal the numbers SURVEY.md §8(a) a5/a6
+    and §8(e) print (computed there by two independent scripts, a numpy one and
+    a scalar C one). Agreement pins the anchors the -m gpu tests assert."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "config_anchors.json")
+    a = json.load(open(p))
+    assert a["c2"]["positions_bytes"] == 1_476_652 and a["c2"]["yp_for_bytes"] == 2_624_044
+    assert a["c4"]["pos1_bytes"] == 66_462_044 and a["c4"]["pos2_bytes"] == 4_719_624
+    c5 = a["c5"]
+    assert c5["positions_bytes"] == 245_585_644 and c5["yp_bytes"] == 677_386_156
+    assert sum(c5["positions_bytes_g8"]) == 245_606_552 and sum(c5["yp_bytes_g8"]) == 677_397_400
+    assert c5["positions_bytes_g8"][0] == 30_699_776 and c5["yp_bytes_g8"][0] == 84_678_464
+    assert c5["shard_counts_g8"] == [33_556_227, 33_555_886, 33_555_972, 33_546_492, 33_560_502, 33_550_630,
+                                     33_557_332, 33_553_873]
+    assert c5["count"] == 268_436_914 and c5["sum_projected"] == 409_182_112_845_958
+    assert a["c3"]["delta_bp2048_payload_bytes"] == 326_463_488 and a["c3"]["static_bp_auto_width"] == 27

@@ -41,7 +41,12 @@ def c2_shard(arg):
     Y = O.encode(synth.gen_host("c2.Y", m, start), O.FOR_BP, 0, 512)
     pos = O.select(X, O.EQ, 17, row_offset=start, out_fmt=O.DELTA_BP, out_block=512)
     yp = O.project(Y, pos, start, O.FOR_BP, 0, 512)
-    return pos.n, O.agg_sum(yp)
+    return pos.n, O.agg_sum(yp), O.decode(pos), O.decode(yp)
+
+
+def image_bytes(values, fmt, block):
+    """Footprint of the oracle's canonical image of `values`."""
+    return O.encode(values, fmt, 0, block).footprint()
 
 
 # ---------------------------------------------------------------- c5
@@ -51,7 +56,21 @@ def c5_shard(arg):
     Y = O.encode(synth.gen_host("c5.Y", m, start), O.FOR_BP, 0, 512)
     pos = O.select(X, O.LT, 1 << 16, row_offset=start, out_fmt=O.DELTA_BP, out_block=512)
     yp = O.project(Y, pos, start, O.FOR_BP, 0, 512)
-    return pos.n, O.agg_sum(yp)
+    return pos.n, O.agg_sum(yp), O.decode(pos), O.decode(yp)
+
+
+def c5_images(res, G):
+    """Footprints of the positions (DELTA_BP{512}) and Y' (FOR_BP{512}) images
+    when the 2^32 rows are cut into G row-range shards (2^24-row pieces in order;
+    G divides 256): per-shard images, encoded from the concatenated decoded
+    pieces of each shard."""
+    per = len(res) // G
+    pos_b, yp_b = [], []
+    for k in range(G):
+        part = res[k * per:(k + 1) * per]
+        pos_b.append(image_bytes(np.concatenate([r[2] for r in part]), O.DELTA_BP, 512))
+        yp_b.append(image_bytes(np.concatenate([r[3] for r in part]), O.FOR_BP, 512))
+    return pos_b, yp_b
 
 
 # ---------------------------------------------------------------- c4 (D-16 chain)
@@ -75,7 +94,7 @@ def c4_shard(arg):
     gid = O.project(gattr, k3p, 0, O.STATIC_BP, 10, 0)
     g1 = O.agg_sum_grouped(gid, m1p, 1000)
     g2 = O.agg_sum_grouped(gid, m2p, 1000)
-    return pos1.n, pos2.n, O.agg_sum(m1p), O.agg_sum(m2p), g1, g2
+    return pos1.n, pos2.n, O.agg_sum(m1p), O.agg_sum(m2p), g1, g2, O.decode(pos1), O.decode(pos2)
 
 
 def run_c4(pool):
@@ -89,7 +108,9 @@ def run_c4(pool):
     return {"n": n, "count_pos1": sum(r[0] for r in res), "count_pos2": sum(r[1] for r in res),
             "sum_m1": sum(r[2] for r in res) & M64, "sum_m2": sum(r[3] for r in res) & M64,
             "bitmap_bits_set": int(sum(bin(int(w)).count("1") for w in synth.bitmap_c4())),
-            "grouped_m1": [int(x) for x in g1], "grouped_m2": [int(x) for x in g2]}
+            "grouped_m1": [int(x) for x in g1], "grouped_m2": [int(x) for x in g2],
+            "pos1_bytes": image_bytes(np.concatenate([r[6] for r in res]), O.DELTA_BP, 512),
+            "pos2_bytes": image_bytes(np.concatenate([r[7] for r in res]), O.DELTA_BP, 512)}
 
 
 # ---------------------------------------------------------------- c3 (whole column)
@@ -109,7 +130,7 @@ def run_c3():
     assert s_r == s_d
     sbp = O.morph(d, O.STATIC_BP, 0, 0)
     return {"n": n, "runs": runs, "rle_runs": r.n_runs, "max": int(x.max()), "static_bp_auto_width": sbp.bit_width,
-            "count": int(pos_d.n), "first": int(pv[0]) if pv.size else None,
+            "sum_all": int(O.agg_sum(d)), "count": int(pos_d.n), "first": int(pv[0]) if pv.size else None,
             "last": int(pv[-1]) if pv.size else None, "sum_selected": int(s_d),
             "delta_bp2048_payload_bytes": int(8 * d.payload.size), "positions_bytes": pos_d.footprint()}
 
@@ -123,15 +144,23 @@ def main():
         if "c2" in which:
             t = time.time()
             res = pool.map(c2_shard, shards(1 << 28))
+            yv = np.concatenate([r[3] for r in res])
             anchors["c2"] = {"n": 1 << 28, "count": sum(r[0] for r in res),
-                             "sum_projected": sum(r[1] for r in res) & M64}
+                             "sum_projected": sum(r[1] for r in res) & M64,
+                             "positions_bytes": image_bytes(np.concatenate([r[2] for r in res]), O.DELTA_BP, 512),
+                             "yp_for_bytes": image_bytes(yv, O.FOR_BP, 512),
+                             "yp_uncompr_bytes": 8 * int(yv.size)}
             print("c2", anchors["c2"], f"{time.time() - t:.0f}s", flush=True)
         if "c5" in which:
             t = time.time()
             res = pool.map(c5_shard, shards(1 << 32))
             per8 = [sum(r[0] for r in res[k * 32:(k + 1) * 32]) for k in range(8)]
+            p1, y1 = c5_images(res, 1)
+            p8, y8 = c5_images(res, 8)
             anchors["c5"] = {"n": 1 << 32, "count": sum(r[0] for r in res),
-                             "sum_projected": sum(r[1] for r in res) & M64, "shard_counts_g8": per8}
+                             "sum_projected": sum(r[1] for r in res) & M64, "shard_counts_g8": per8,
+                             "positions_bytes": p1[0], "yp_bytes": y1[0],
+                             "positions_bytes_g8": p8, "yp_bytes_g8": y8}
             print("c5", anchors["c5"], f"{time.time() - t:.0f}s", flush=True)
         if "c4" in which:
             t = time.time()
