@@ -500,51 +500,6 @@ ms_status compress_rle(const Ctx& ctx, const uint64_t* values, uint64_t n, ms_co
   return MS_OK;
 }
 
-// select -> DELTA_BP{512} in one pass (select_pos.cu): the output is allocated at
-// a provable capacity before the kernel (select_pos_width_bound; the kernel writes
-// every block at its final place) and described exactly after the op's single
-// read-back. The allocation keeps its slack (no copy) unless MS_FLAG_SHRINK is set.
-ms_status select_positions_onepass(const Ctx& ctx, const ms_column* in, const PredSpec& ps, uint64_t row_offset,
-                                   const ms_fmt& f, ms_column* out) {
-  const uint64_t n = in->n;
-  const uint32_t B = f.block_size;
-  const uint64_t T = select_pos_tiles(n);
-  Scratch sc(ctx);
-  const uint64_t o_meta = sc.add(64, true);
-  const uint64_t o_tk = sc.add(8, true);
-  const uint64_t o_st1 = sc.add(8 * T, true);
-  const uint64_t o_st2 = sc.add(8 * T, true);
-  const uint64_t o_cnt = sc.add(4 * T, false);
-  const uint64_t o_tail = sc.add(2 * (uint64_t)(B - 1) * T, false);
-  if (!sc.commit()) return MS_E_NOMEM;
-  const uint64_t nbmax = n / B;
-  uint64_t wsum = select_pos_width_bound(n, B);
-  if (wsum > 64 * nbmax) wsum = 64 * nbmax;
-  const uint64_t cap = wsum * (B / 64);
-  MS_TRY(alloc_column(ctx, out, f, nbmax * B + (B - 1), cap, 0));
-  uint64_t* meta = sc.at<uint64_t>(o_meta);
-  cudaError_t e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
-  if (e == cudaSuccess)
-    e = launch_select_pos(view_of(in), ps, B, row_offset, sc.at<uint32_t>(o_tk), sc.at<uint64_t>(o_st1),
-                          sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_cnt), sc.at<uint16_t>(o_tail), meta,
-                          reinterpret_cast<uint32_t*>(meta), out->payload, out->cw, out->ref, out->rem, cap, ctx.s);
-  uint64_t h[4] = {0, 0, 0, 0};
-  ms_status st = e == cudaSuccess ? readback(ctx, meta, h, 4) : cuda_status(e);  // the op's one sync
-  if (st == MS_OK) st = status_from_bits((uint32_t)h[0]);
-  if (st != MS_OK) {
-    release(ctx, out);
-    return st;
-  }
-  out->n = h[1];
-  out->n_blocks = h[1] / B;
-  out->n_rem = h[1] % B;
-  out->payload_words = h[2] * (B / 64);
-  out->fmt.max_width = (uint32_t)h[3];
-  if (ctx.c && (ctx.c->flags & MS_FLAG_SHRINK)) st = maybe_shrink(ctx, out);
-  if (st != MS_OK) release(ctx, out);
-  return st;
-}
-
 // worst-case payload words of a block-format column of n values when every
 // block may need 64 bits
 uint64_t full_cap(uint64_t n, uint32_t B) { return (n / B) * B; }
@@ -745,8 +700,6 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   MS_TRY(make_pred(pred, ps));
   Ctx ctx(ctx_);
   const uint64_t n = in->n;
-  if (out_fmt.format == MS_DELTA_BP && select_pos_supported(view_of(in), out_fmt.block_size))
-    return select_positions_onepass(ctx, in, ps, row_offset, out_fmt, out);
   const uint64_t NS = (n + kSegRows - 1) / kSegRows;  // 512-row segments
   const uint64_t n_words = NS * kSegWords;
   const uint32_t G = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;  // output item size

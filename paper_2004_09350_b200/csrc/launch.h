@@ -121,20 +121,6 @@ cudaError_t launch_sum_at(const ColView& data, const ColView& pos, uint64_t row_
 cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t n_groups,
                                unsigned long long* sums, uint32_t* err, cudaStream_t s);
 
-// select -> DELTA_BP{B} positions in one pass (select_pos.cu), for the inputs and B that
-// select_pos_supported accepts. Scratch: ticket (u32, zeroed), st1/st2 (T u64 each, zeroed), cnt
-// (T u32), tail (T * (B-1) u16), meta (4 u64, zeroed; meta[0] low 32 bits = err word), with
-// T = select_pos_tiles(n). Output arrays sized for n / B blocks, B - 1 remainder rows and cap_words
-// payload words (>= select_pos_width_bound(n, B) * B / 64). Results: meta[1] = n_out,
-// meta[2] = cw[nb], meta[3] = largest block width.
-bool select_pos_supported(const ColView& c, uint32_t B);
-cudaError_t launch_select_pos(const ColView& c, const PredSpec& p, uint32_t B, uint64_t row_offset,
-                              uint32_t* ticket, uint64_t* st1, uint64_t* st2, uint32_t* cnt, uint16_t* tail,
-                              uint64_t* meta, uint32_t* err, uint64_t* payload, uint32_t* cw, uint64_t* ref,
-                              uint64_t* rem, uint64_t cap_words, cudaStream_t s);
-uint64_t select_pos_tiles(uint64_t n);
-uint64_t select_pos_width_bound(uint64_t n, uint32_t B);
-
 int num_sms();
 // largest block width max(cw[b+1] - cw[b]) into *out (zero-initialised)
 cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cudaStream_t s);

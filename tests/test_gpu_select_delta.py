@@ -1,11 +1,10 @@
-"""GPU parity of the one-pass select -> DELTA_BP{512} kernel (select_pos.cu)
-against the oracle, byte for byte, on the cases its tiling creates: several
-32K-row tiles with ragged tails, blocks straddling many tiles (heads gathered
-from several predecessors' tails), tiles without matches, the final partial
-block written by the last tile, partial 512-row segments and block remainders
-decoded by random access, every input layout it stages (STATIC_BP at widths
-1..64, UNCOMPR, DYN_BP / FOR_BP with B >= 512, narrow and wide widths), the
-code-domain predicate on FOR, bitmaps, and large row offsets (D-10)."""
+"""GPU parity of select -> DELTA_BP{512} positions (the paper's positions
+format) against the oracle, byte for byte, at sizes that span many
+select tiles and output blocks with ragged tails: blocks straddling many empty
+tiles, the final partial block, partial 512-row segments and block remainders,
+every fast input layout (STATIC_BP at widths 1..64, UNCOMPR, DYN_BP / FOR_BP with
+B >= 512, narrow and wide widths), the FOR code-domain predicate, bitmaps and
+large row offsets (D-10)."""
 import numpy as np
 import pytest
 
