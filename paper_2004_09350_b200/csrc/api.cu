@@ -45,12 +45,6 @@ struct Ctx {
   }
 };
 
-// experiment switches (measured alternatives; defaults are the measured-best paths)
-bool env_flag(const char* name) {
-  const char* v = getenv(name);
-  return v && *v && *v != '0';
-}
-
 // One scratch allocation per op, carved into 256-byte aligned regions.
 struct Scratch {
   const Ctx& ctx;
@@ -421,7 +415,7 @@ ms_status encode_into(const Ctx& ctx, Scratch& sc, uint64_t meta_off, uint64_t s
   const uint64_t n_tiles = (n + kChunk - 1) / kChunk, nb = is_block(fmt.format) ? n / fmt.block_size : 0;
   // (8 bytes per row of slots; when they cannot be allocated the engine falls back
   // to the in-order look-back, which needs no slots)
-  bool slot_mode = nb && !env_flag("MS_ENGINE_LOOKBACK");
+  bool slot_mode = nb != 0;
   void* slot_mem = nullptr;
   uint64_t *cwx = nullptr, *scan_st = nullptr;
   uint32_t* scan_tk = nullptr;
@@ -617,7 +611,7 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
     }
     return MS_OK;
   }
-  if (in->fmt.format == MS_RLE && fmt.format == MS_DELTA_BP && !env_flag("MS_MORPH_ENGINE")) {
+  if (in->fmt.format == MS_RLE && fmt.format == MS_DELTA_BP) {
     // direct morph: from the runs alone (morph.cu)
     const uint32_t B = fmt.block_size;
     const uint64_t nb = n / B, nrem = n % B;
@@ -715,8 +709,7 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t o_tk1 = sc.add(8, true);
   const bool pos_delta = out_fmt.format == MS_DELTA_BP && G <= 512;  // posdelta.cuh
   // other formats with items <= 512: the slot encoder (MaskSource), no look-back
-  const bool pos_slots = !pos_delta && G <= 512 && out_fmt.format != MS_RLE && !env_flag("MS_ENCODE_TICKET") &&
-                         !env_flag("MS_POS_DEFERRED");
+  const bool pos_slots = !pos_delta && G <= 512 && out_fmt.format != MS_RLE;
   const uint64_t o_st2 = sc.add(pos_delta || pos_slots ? 8 : 8 * (items_max + 1), true);  // look-back status
   const uint64_t o_tk2 = sc.add(8, true);
   const bool wscan = pos_delta || pos_slots;
@@ -792,7 +785,7 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
     // wcap = ebw(NS * 512 - 1) bits per code bound every block (B * wcap / 64 words per slot)
     uint64_t* slots = nullptr;
     uint32_t slot_words = 0;
-    if (pos_delta && f.format == MS_DELTA_BP && !env_flag("MS_POS_TWO_WALKS")) {
+    if (pos_delta && f.format == MS_DELTA_BP) {
       const uint32_t wcap = ebw_host(NS * kSegRows - 1);
       slot_words = G / 64 * (wcap ? wcap : 1);
       slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
@@ -837,26 +830,8 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
   if (out_fmt.format == MS_RLE) return MS_E_UNSUPPORTED;
   Ctx ctx(ctx_);
   const uint64_t n = positions->n;
-  // DELTA_BP / RLE data have no O(1) row access (D-12). When the positions are dense
-  // enough that the gather would decode most data tiles anyway (>= 1 per 64 rows),
-  // decode the column once (staged engine / rle_expand) and gather from its rows.
-  if ((data->fmt.format == MS_DELTA_BP || data->fmt.format == MS_RLE) && data->n && n * 64 >= data->n &&
-      8 * data->n <= (4ull << 30) && !env_flag("MS_PROJECT_NO_EXPAND")) {
-    uint64_t* tmp = (uint64_t*)ctx.alloc(8 * data->n);
-    if (tmp) {
-      ms_status st = ms_decompress(ctx_, data, tmp);
-      if (st == MS_OK) {
-        ms_column u{};
-        u.fmt = ms_fmt{MS_UNCOMPR, 0, 0, 0};
-        u.n = data->n;
-        u.payload_words = data->n;
-        u.payload = tmp;
-        st = ms_project(ctx_, &u, positions, row_offset, out_fmt, out);  // synchronises before returning
-      }
-      ctx.free(tmp);
-      return st;
-    }
-  }
+  // DELTA_BP / RLE data have no O(1) row access (D-12): the gather engine decodes
+  // only the data tiles a positions tile spans (no whole-column materialisation, DP3)
   if (is_block(out_fmt.format) && 64 * (n / out_fmt.block_size) > 0xffffffffull) return MS_E_INVALID;
   const uint64_t items = (n + 127) / 128;  // enough for any item size (>= 128 rows)
   // the slot path (no look-back status) serves item sizes <= 512 into block formats or UNCOMPR
@@ -867,9 +842,7 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
                          (df0 == MS_UNCOMPR || df0 == MS_STATIC_BP || df0 == MS_DYN_BP || df0 == MS_FOR_BP) &&
                          !(out_fmt.format == MS_STATIC_BP && out_fmt.bit_width == 0);
   const bool slot_path = warp_path && G0 <= 512 &&
-                         (is_block(out_fmt.format) || out_fmt.format == MS_UNCOMPR || out_fmt.format == MS_STATIC_BP) &&
-                         !env_flag("MS_PROJECT_DEFERRED") && !env_flag("MS_PROJECT_PIPE") &&
-                         !env_flag("MS_PROJECT_WIN") && !env_flag("MS_ENCODE_TICKET");
+                         (is_block(out_fmt.format) || out_fmt.format == MS_UNCOMPR || out_fmt.format == MS_STATIC_BP);
   Scratch sc(ctx);
   const uint64_t o_meta = sc.add(64, true);
   const uint64_t o_st = sc.add(slot_path ? 8 : 8 * (items + 1), true);

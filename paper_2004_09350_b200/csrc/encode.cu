@@ -4,8 +4,6 @@
 #include "grid.cuh"
 #include "positions.cuh"
 #include "posdelta.cuh"
-#include "project.cuh"
-#include "projwin.cuh"
 #include "launch.h"
 
 namespace ms {
@@ -14,18 +12,16 @@ namespace ms {
 template <class Src>
 static cudaError_t run_warp_encode(const Src& src, const PosEnc& e0, uint64_t* status, uint32_t* ticket,
                                    uint32_t* err, const char* name, cudaStream_t s) {
-  PosEnc e = e0;
-  e.exp = (uint32_t)env_int("MS_EXP", 0);
+  const PosEnc& e = e0;
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   if (!n_items) return cudaSuccess;
-  if (e.G <= 512 && !env_int("MS_ENCODE_TICKET", 0)) {  // deferred look-back, two tiles per warp
+  if (e.G <= 512) {  // deferred look-back, two tiles per warp
     auto launch = [&](auto k) {
       const int warps = 4;
       const size_t smem = (size_t)warps * 2 * tile_slots(e.G) * 8;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
-  if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
       if (per_sm < 1) per_sm = 1;
       uint64_t grid = (uint64_t)per_sm * num_sms();
       const uint64_t need = (n_items + warps - 1) / warps;
@@ -44,7 +40,6 @@ static cudaError_t run_warp_encode(const Src& src, const PosEnc& e0, uint64_t* s
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
-  if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)per_sm * num_sms();
   const uint64_t need = (n_items + warps - 1) / warps;
@@ -90,24 +85,11 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
     r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
     if (r != cudaSuccess) return r;
     uint64_t cgrid = (n_full + 31) / 32;  // 8 lanes per block
-    if (cgrid > (uint64_t)env_int("MS_COPY_CTAS", 1 << 20)) cgrid = (uint64_t)env_int("MS_COPY_CTAS", 1 << 20);
     ProfScope prof_("pos_copy", s);
     pos_copy_kernel<8><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
     return cudaGetLastError();
   }
-  if (n_full) {
-    const size_t smem = (size_t)kPdWarps * kPdStageU32 * 4;
-    const int grid = grid_for(pos_width_kernel, smem, n_full);
-    {
-      ProfScope prof_("pos_width", s);
-      pos_width_kernel<<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e.G, n_full, n_items,
-                                                          wk, err);
-    }
-    cudaError_t r = cudaGetLastError();
-    if (r != cudaSuccess) return r;
-    r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
-    if (r != cudaSuccess) return r;
-  }
+  // no full block: the remainder alone (raw positions)
   const size_t smem = (size_t)kPdWarps * kPdWarpU32 * 4;
   const int grid = grid_for(pos_pack_kernel, smem, n_items);
   ProfScope prof_("pos_pack", s);
@@ -117,76 +99,9 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
 
 cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                 uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s) {
-  // register-resident path: DELTA_BP{G} positions, header-addressed data, block output of size G or UNCOMPR
-  const bool out_block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
-  const uint32_t pf = (uint32_t)env_int("MS_GATHER_PREFETCH", 1);
-  if (pos.format == MS_DELTA_BP && pos.B == e.G && e.G >= 128 && e.G <= 512 &&
-      (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && (out_block || e.format == MS_UNCOMPR) &&
-      env_int("MS_PROJECT_WIN", 0)) {
-    const uint64_t n_full = e.n_out / e.G;
-    if (n_full) {
-      auto launch = [&](auto k) {
-        const size_t smem = 2 * (size_t)kWinSlotBytes + 3 * (size_t)tile_slots(e.G) * 8;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem);
-        if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
-        if (per_sm < 1) per_sm = 1;
-        uint64_t grid = (uint64_t)per_sm * num_sms();
-        if (n_full < grid) grid = n_full;
-        ProfScope prof_("project_win", s);
-        k<<<(int)grid, 32, smem, s>>>(pos, data, row_offset, e, n_full, status, err);
-        return cudaGetLastError();
-      };
-      cudaError_t r = e.G == 512   ? launch(project_win_kernel<16>)
-                      : e.G == 256 ? launch(project_win_kernel<8>)
-                                   : launch(project_win_kernel<4>);
-      if (r != cudaSuccess) return r;
-    }
-    if (n_full * e.G < e.n_out) {
-      ProfScope prof_("project_tail", s);
-      project_tail_kernel<<<1, 256, 0, s>>>(pos, data, row_offset, e, n_full * e.G, err);
-    }
-    return cudaGetLastError();
-  }
-  if (pos.format == MS_DELTA_BP && pos.B == e.G && e.G >= 128 && e.G <= 512 &&
-      (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && (out_block || e.format == MS_UNCOMPR) &&
-      env_int("MS_PROJECT_PIPE", 0)) {
-    const uint64_t n_full = e.n_out / e.G;
-    if (n_full) {
-      auto launch = [&](auto k) {
-        const int warps = 4;
-        const size_t smem = (size_t)warps * 3 * tile_slots(e.G) * 8;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
-        if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
-        if (per_sm < 1) per_sm = 1;
-        uint64_t grid = (uint64_t)per_sm * num_sms();
-        const uint64_t need = (n_full + warps - 1) / warps;
-        if (need < grid) grid = need;
-        ProfScope prof_("project_pipe", s);
-        k<<<(int)grid, warps * 32, smem, s>>>(pos, data, row_offset, e, n_full, status, err, pf);
-        return cudaGetLastError();
-      };
-      cudaError_t r = e.G == 512   ? launch(project_pipe_kernel<16>)
-                      : e.G == 256 ? launch(project_pipe_kernel<8>)
-                                   : launch(project_pipe_kernel<4>);
-      if (r != cudaSuccess) return r;
-    }
-    if (n_full * e.G < e.n_out) {
-      ProfScope prof_("project_tail", s);
-      project_tail_kernel<<<1, 256, 0, s>>>(pos, data, row_offset, e, n_full * e.G, err);
-    }
-    return cudaGetLastError();
-  }
-  // tuning knobs (defaults measured on B200; env overrides are for experiments)
-  const int batch = env_int("MS_GATHER_BATCH", 4);
-  if (batch >= 16) return run_warp_encode(ProjectSource<16>{pos, data, row_offset, pf}, e, status, ticket, err,
-                                          "project_warp", s);
-  if (batch >= 8) return run_warp_encode(ProjectSource<8>{pos, data, row_offset, pf}, e, status, ticket, err,
-                                         "project_warp", s);
-  return run_warp_encode(ProjectSource<4>{pos, data, row_offset, pf}, e, status, ticket, err, "project_warp", s);
+  // gather + encode with a look-back on the output widths (items > 512, or outputs the slot path
+  // does not serve); 4 independent gathers in flight per lane, one bulk L2 prefetch per window
+  return run_warp_encode(ProjectSource<4>{pos, data, row_offset, 1u}, e, status, ticket, err, "project_warp", s);
 }
 
 // select positions in a format other than DELTA_BP (items <= 512): MaskSource into
@@ -222,7 +137,6 @@ cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64
   r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
   if (r != cudaSuccess) return r;
   uint64_t cgrid = (n_full + 31) / 32;  // 8 lanes per block
-  if (cgrid > (uint64_t)env_int("MS_COPY_CTAS", 1 << 20)) cgrid = (uint64_t)env_int("MS_COPY_CTAS", 1 << 20);
   ProfScope prof_("pos_copy", s);
   pos_copy_kernel<8><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
   return cudaGetLastError();
@@ -233,20 +147,18 @@ cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64
 cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e0,
                                  uint64_t* slots, uint32_t slot_words, uint32_t* wk, uint64_t* cwx,
                                  uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err, cudaStream_t s) {
-  PosEnc e = e0;
-  e.exp = 0;
+  const PosEnc& e = e0;
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   const uint64_t n_full = e.n_out / e.G;
   if (!n_items) return cudaSuccess;
-  const uint32_t pf = (uint32_t)env_int("MS_GATHER_PREFETCH", 1);
+  const uint32_t pf = 1;  // one bulk L2 prefetch of each data window
   auto launch = [&](auto k, auto src) {
     const int warps = 4;
     const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
-    if (const int cap = env_int("MS_ENCODE_CTAS_PER_SM", 0)) per_sm = per_sm < cap ? per_sm : cap;
-    if (per_sm < 1) per_sm = 1;
+      if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)per_sm * num_sms();
     const uint64_t need = (n_items + warps - 1) / warps;
     if (need < grid) grid = need;
@@ -264,7 +176,6 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
   r = launch_count_scan(wk, n_full, cwx, scan_status, scan_ticket, s);
   if (r != cudaSuccess) return r;
   uint64_t cgrid = (n_full + 7) / 8;
-  if (cgrid > (uint64_t)env_int("MS_COPY_CTAS", 1 << 20)) cgrid = (uint64_t)env_int("MS_COPY_CTAS", 1 << 20);
   ProfScope prof_("project_copy", s);
   pos_copy_kernel<32><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
   return cudaGetLastError();

@@ -17,10 +17,5 @@ static inline int persistent_grid(K kernel, int threads, uint64_t items) {
   return (int)(g ? g : 1);
 }
 
-static inline int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 
 }  // namespace ms

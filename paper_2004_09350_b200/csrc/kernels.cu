@@ -137,8 +137,7 @@ cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* 
   // staged input (stage.cuh) whenever tiles go in a static order: every output but
   // a block format written with the look-back
   const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP);
-  static const bool unstaged = getenv("MS_ENGINE_UNSTAGED") != nullptr;
-  if (stageable_format(src.format) && !out.n_dev && !ordered && !unstaged) {
+  if (stageable_format(src.format) && !out.n_dev && !ordered) {
     const bool max_only = out.format == OUT_MAX_ONLY;
     switch (src.format) {
       case MS_UNCOMPR: return launch_staged<MS_UNCOMPR>(src, out, err, max_only, s);
@@ -320,7 +319,7 @@ static cudaError_t run_scan(In in, Epi epi, uint64_t N, uint64_t* status, uint32
   if (N == 0) return cudaSuccess;
   const uint64_t T = (N + kChunk - 1) / kChunk;
   ProfScope prof_("scan", s);
-  if (T > 1 && !env_int("MS_SCAN_LOOKBACK", 0)) {  // status holds >= T + 1 entries
+  if (T > 1) {  // reduce-then-scan (status holds >= T + 1 entries); one tile: a single kernel
     auto kr = scan_reduce_kernel<In>;
     auto ka = scan_apply_kernel<In, Epi>;
     kr<<<persistent_grid(kr, kThreads, T), kThreads, 0, s>>>(in, N, status);

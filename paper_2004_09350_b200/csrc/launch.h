@@ -66,7 +66,6 @@ struct PosEnc {  // output of the warp encoder
   uint32_t* cw;
   uint64_t* ref;
   uint64_t* rem;
-  uint32_t exp;  // measurement experiments only (MS_EXP), 0 in normal operation
 };
 cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                              uint64_t row_offset, uint64_t* status, uint32_t* ticket, uint32_t* err, cudaStream_t s);

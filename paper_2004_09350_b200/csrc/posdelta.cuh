@@ -290,33 +290,8 @@ __device__ __forceinline__ bool pd_span(const uint64_t* gstart, uint64_t item, u
   return *span + 4 <= kPdStageU32;
 }
 
-// Pass 1: w_k for every full block k < n_full.
-__global__ void __launch_bounds__(kPdWarps * 32) pos_width_kernel(const uint32_t* __restrict__ bits,
-                                                                  uint64_t n_words,
-                                                                  const uint64_t* __restrict__ gstart,
-                                                                  uint64_t row_offset, uint32_t B, uint64_t n_full,
-                                                                  uint64_t n_items, uint32_t* wk, uint32_t* err) {
-  extern __shared__ __align__(16) uint32_t pd_sm[];  // per warp: stage
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t* stage = pd_sm + (size_t)wid * kPdStageU32;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
-  for (uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid; item < n_full; item += nwarps) {
-    const uint64_t row0 = __ldg(gstart + item) - row_offset;
-    uint64_t span;
-    uint32_t w;
-    if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
-      w = B == 512   ? pd_fast_item<16, false>(bits, n_words, row0, span, 0, stage, nullptr, lane)
-          : B == 256 ? pd_fast_item<8, false>(bits, n_words, row0, span, 0, stage, nullptr, lane)
-                     : pd_fast_item<4, false>(bits, n_words, row0, span, 0, stage, nullptr, lane);
-      __syncwarp();
-    } else {
-      w = ebw64(warp_max(pd_walk<false>(bits, n_words, row0, B, 0, nullptr, nullptr, row_offset, lane, err)));
-    }
-    if (lane == 0) wk[item] = w;
-  }
-}
-
-// Pass 2: pack every block at cw[k] = cwx[k] (exclusive prefix of the widths).
+// A walk that packs every block at cw[k] = cwx[k] (exclusive prefix of the widths);
+// launched for outputs without a full block, where it writes the raw remainder.
 __global__ void __launch_bounds__(kPdWarps * 32) pos_pack_kernel(const uint32_t* __restrict__ bits,
                                                                  uint64_t n_words,
                                                                  const uint64_t* __restrict__ gstart,

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosE
   uint64_t prev = ~0ull, prev_ref = 0;
   uint32_t prev_w = 0, cur = 0;
   auto store = [&](uint64_t item, uint32_t w, uint64_t ref, const uint64_t* T) {
-    const uint64_t E = (e.exp & 2) ? item * w : lookback_resolve(status, item, w);  // bit 1: experiment
+    const uint64_t E = lookback_resolve(status, item, w);
     if (lane == 0) {
       if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
       e.cw[item + 1] = (uint32_t)(E + w);
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosE
     uint64_t* P = tiles + cur * tile_slots(G);
     const uint64_t r0 = (uint64_t)item * G;
     const uint32_t cnt = (uint32_t)min((uint64_t)G, e.n_out - r0);
-    if (!(e.exp & 1)) src.load(item, r0, cnt, P, lane, err);  // bit 0: experiment, no source
+    src.load(item, r0, cnt, P, lane, err);
     if (!is_block || cnt < G) {  // no prefix needed
       encode_finish<Src>(e, item, P, cnt, 0, 0, status, err, lane);
       __syncwarp();

@@ -269,7 +269,7 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
     // per pair, 6 CTAs/SM), medium (<= 48 bits, 4 CTAs/SM) or wide (3 CTAs/SM). Measured on B200
     // (BJ.c5): 3-stage and 8-warp variants of the narrow kernel were 8-50% slower.
     const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
-    const bool medium = !narrow && c.maxw >= 33 && c.maxw <= 48 && !env_int("MS_SELECT_NO_MEDIUM", 0);
+    const bool medium = !narrow && c.maxw >= 33 && c.maxw <= 48;
 #define MS_PICK(K)                                                                                   \
   do {                                                                                               \
     if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow);          \

@@ -100,23 +100,6 @@ def test_many_tiles_per_cta(kind, rng):
             assert_same_image(ms.morph(ga, b), O.morph(oa, *oracle_fmt(b)), f"morph {a}->{b} {kind} n={n}")
 
 
-@pytest.mark.parametrize("kind", ["sorted", "outlier", "wide"])
-def test_engine_lookback_fallback(kind, rng, monkeypatch):
-    """Block-format outputs through the in-order look-back engine (the fallback when
-    the per-tile slots cannot be allocated; forced by MS_ENGINE_LOOKBACK)."""
-    ms = get_ms()
-    monkeypatch.setenv("MS_ENGINE_LOOKBACK", "1")
-    n = (1 << 20) + 777
-    v = rand_values(n, kind, rng)
-    t = to_torch(v)
-    for f in (ms.dyn_bp(512), ms.for_bp(128), ms.delta_bp(2048)):
-        oc = O.encode(v, *oracle_fmt(f))
-        gc = ms.compress(t, f)
-        assert_same_image(gc, oc, f"lookback compress {f} {kind}")
-        for b in (ms.delta_bp(256), ms.dyn_bp(1024)):
-            assert_same_image(ms.morph(gc, b), O.morph(oc, *oracle_fmt(b)), f"lookback morph {f}->{b} {kind}")
-
-
 PREDS = None
 
 
@@ -192,15 +175,15 @@ def test_project(kind, rng):
                     assert_same_image(gr, orr, f"project {fd} @ {fp} -> {fo} {kind}")
 
 
-def test_project_sequential_data_gather(rng, monkeypatch):
-    """DELTA_BP / RLE data gathered tile by tile (the path for sparse positions; dense
-    positions decode the column first, which test_project covers)."""
+@pytest.mark.parametrize("density", [3000, 9000])
+def test_project_sequential_data_gather(rng, density):
+    """DELTA_BP / RLE data gathered tile by tile (no whole-column decode, DP3),
+    sparse and dense positions."""
     ms = get_ms()
-    monkeypatch.setenv("MS_PROJECT_NO_EXPAND", "1")
     n = 5 * 2048 + 13
     v = rand_values(n, "sorted", rng)
     t = to_torch(v)
-    pos = np.sort(rng.choice(n, 3000, replace=False)).astype(np.uint64)
+    pos = np.sort(rng.choice(n, density, replace=False)).astype(np.uint64)
     for fd in (ms.delta_bp(128), ms.delta_bp(2048), ms.rle()):
         gd = ms.compress(t, fd)
         od = O.encode(v, *oracle_fmt(fd))

@@ -1,7 +1,8 @@
 """GPU parity of select's positions encoder (mask -> DELTA_BP{B}, posdelta.cuh)
-against the oracle, bit-exact, across the selectivities that switch between its
-two paths (dense masks: rank-per-lane fast path; sparse masks: the walker), every
-block size it serves, block-boundary tails and large row offsets."""
+against the oracle, bit-exact, across the selectivities that switch between the
+two walks of pos_slot (dense masks: rank-per-lane fast path; sparse masks: the
+round-based walker), every block size it serves, block-boundary tails and large
+row offsets; other positions formats through the slot and look-back encoders."""
 import numpy as np
 import pytest
 
@@ -13,17 +14,8 @@ pytestmark = pytest.mark.gpu
 SELECTIVITY = [1.0, 0.9, 0.5, 0.0625, 0.02, 0.0155, 0.005, 0.0003]
 
 
-@pytest.fixture(params=["slots", "two_walks"])
-def walk(request, monkeypatch):
-    """Both encoder pipelines: single walk into slots + copy (default), or
-    width walk + pack walk (MS_POS_TWO_WALKS=1)."""
-    if request.param == "two_walks":
-        monkeypatch.setenv("MS_POS_TWO_WALKS", "1")
-    return request.param
-
-
 @pytest.mark.parametrize("sel", SELECTIVITY)
-def test_positions_delta_bp(sel, walk):
+def test_positions_delta_bp(sel):
     ms = get_ms()
     rng = np.random.default_rng(int(sel * 1e6) + 7)
     for n in (600_001, 512 * 1024):
@@ -38,7 +30,7 @@ def test_positions_delta_bp(sel, walk):
                 assert_same_image(g, o, f"sel={sel} n={n} B={B} off={off}")
 
 
-def test_positions_clustered(walk):
+def test_positions_clustered():
     """Matches in dense clusters separated by long gaps: blocks mix both paths
     within one CTA tile."""
     ms = get_ms()
@@ -55,13 +47,10 @@ def test_positions_clustered(walk):
         assert_same_image(g, o, f"clustered B={B}")
 
 
-@pytest.mark.parametrize("deferred", [False, True])
 @pytest.mark.parametrize("sel", [0.9, 0.0625, 0.003])
-def test_positions_other_formats(sel, deferred, monkeypatch):
-    """Positions as UNCOMPR / STATIC_BP / DYN_BP / FOR_BP (slot encoder, or the
-    deferred look-back encoder with MS_POS_DEFERRED=1), byte-exact."""
-    if deferred:
-        monkeypatch.setenv("MS_POS_DEFERRED", "1")
+def test_positions_other_formats(sel):
+    """Positions as UNCOMPR / STATIC_BP / DYN_BP / FOR_BP / RLE (slot encoder, and
+    the deferred look-back encoder for RLE), byte-exact."""
     ms = get_ms()
     rng = np.random.default_rng(int(sel * 1000) + 3)
     n = 400_003
@@ -71,8 +60,9 @@ def test_positions_other_formats(sel, deferred, monkeypatch):
     oX = O.encode(v, O.DYN_BP, 0, 512)
     for fo, of in ((ms.uncompr(), (O.UNCOMPR, 0, 0)), (ms.static_bp(0), (O.STATIC_BP, 0, 0)),
                    (ms.static_bp(40), (O.STATIC_BP, 40, 0)), (ms.dyn_bp(512), (O.DYN_BP, 0, 512)),
-                   (ms.for_bp(256), (O.FOR_BP, 0, 256)), (ms.dyn_bp(128), (O.DYN_BP, 0, 128))):
+                   (ms.for_bp(256), (O.FOR_BP, 0, 256)), (ms.dyn_bp(128), (O.DYN_BP, 0, 128)),
+                   (ms.dyn_bp(2048), (O.DYN_BP, 0, 2048)), (ms.rle(), (O.RLE, 0, 0))):
         for off in (0, 1 << 33):
             g = ms.select(X, ms.LT, thr, row_offset=off, out_fmt=fo)
             o = O.select(oX, O.LT, thr, row_offset=off, out_fmt=of[0], out_width=of[1], out_block=of[2] or 512)
-            assert_same_image(g, o, f"sel={sel} -> {fo} off={off} deferred={deferred}")
+            assert_same_image(g, o, f"sel={sel} -> {fo} off={off}")

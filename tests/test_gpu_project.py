@@ -1,9 +1,10 @@
-"""GPU parity of project's register-resident path (project.cuh: DELTA_BP{G}
-positions -> DYN_BP / FOR_BP data -> block output of size G or UNCOMPR)
-against the oracle, bit-exact: densities that do and do not fit the 32-block
-data window, data blocks wider than 32 bits, unsorted and repeated positions,
-positions in the data remainder, a final partial positions block, and the
-range error."""
+"""GPU parity of project's gather encoders (positions.cuh ProjectSource:
+DELTA_BP{G} positions -> DYN_BP / FOR_BP data -> block output of size G or
+UNCOMPR; G <= 512 through the slot encoder, larger G through the look-back
+encoder) against the oracle, bit-exact: densities that do and do not fit the
+32-block data window, data blocks wider than 32 bits, unsorted and repeated
+positions, positions in the data remainder, a final partial positions block, and
+the range error."""
 import numpy as np
 import pytest
 
@@ -12,15 +13,10 @@ from tests.gpu_util import assert_same_image, get_ms, oracle_fmt, to_torch
 
 pytestmark = pytest.mark.gpu
 
-# the encoder paths project can take for these inputs (env switches read at launch)
-PATHS = {"default": {}, "deferred": {"MS_PROJECT_DEFERRED": "1"}, "pipe": {"MS_PROJECT_PIPE": "1"},
-         "ticketed": {"MS_ENCODE_TICKET": "1"}, "window": {"MS_PROJECT_WIN": "1"}}
-
-
-@pytest.fixture(params=sorted(PATHS))
-def path(request, monkeypatch):
-    for k, v in PATHS[request.param].items():
-        monkeypatch.setenv(k, v)
+@pytest.fixture(params=["slots", "lookback"])
+def path(request):
+    """Output block size 512 goes through the slot encoder (no look-back); 1024
+    through the look-back encoder (warp_encode_kernel)."""
     return request.param
 
 
@@ -47,7 +43,7 @@ def test_project_fast(kind, density, path):
     for fd in (ms.for_bp(512), ms.dyn_bp(512), ms.for_bp(128), ms.dyn_bp(2048)):
         gd = ms.compress(to_torch(v), fd)
         od = O.encode(v, *oracle_fmt(fd))
-        for G in (512, 128):
+        for G in ((512, 128) if path == "slots" else (1024, 2048)):
             fp = ms.delta_bp(G)
             gp = ms.compress(to_torch(sel), fp)
             op_ = O.encode(sel, *oracle_fmt(fp))
@@ -58,7 +54,7 @@ def test_project_fast(kind, density, path):
                 assert_same_image(gr, orr, f"project {kind} d={density} {fd} @ DELTA_BP{{{G}}} -> {fo}")
 
 
-def test_project_fast_unsorted_and_repeated(path):
+def test_project_fast_unsorted_and_repeated():
     ms = get_ms()
     rng = np.random.default_rng(11)
     n = 100_000
@@ -74,7 +70,7 @@ def test_project_fast_unsorted_and_repeated(path):
         assert_same_image(ms.project(gd, gp, 0, fo), O.project(od, op_, 0, *oracle_fmt(fo)), f"-> {fo}")
 
 
-def test_project_fast_range_error(path):
+def test_project_fast_range_error():
     ms = get_ms()
     v = np.arange(5000, dtype=np.uint64)
     gd = ms.compress(to_torch(v), ms.for_bp(512))
