@@ -13,8 +13,11 @@ Inputs are seeded synthetic columns (synth/), generated on
 the device shard by shard and compressed by libms before the timed region.
 Inputs (10.8 + 10.9 GB at N=1) are far larger than L2 (126 MB): no L2 flush.
 
-usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5|c2|c3|c1]
+usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+(or plain `python bench.py --gpus N`: without WORLD_SIZE in the environment the
+script re-launches itself under torch.distributed.run, one rank per GPU, with
+NCCL_DEBUG=INFO unless set).
 """
 from __future__ import annotations
 
@@ -55,6 +58,36 @@ def parse():
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
         os.environ.get("LOCAL_RANK", "0"))
+
+
+NOMINAL_HBM_GBS = 8000.0  # BASELINE.json north_star's "~8 TB/s"
+
+
+def host_info():
+    """The host the CPU legs run on: logical CPUs, model name, and the pinning used."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+class pinned_to_one_core:
+    """Pin this process to one CPU for the oracle timing (the paper's single-thread
+    setup); restores the previous affinity."""
+
+    def __enter__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.cpu = min(self.prev)
+        os.sched_setaffinity(0, {self.cpu})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.prev)
 
 
 def peaks():
@@ -141,12 +174,13 @@ def run_reference(args):
         return 0
     n_s = 1 << 22
     X, Y = oracle_sample(n_s)
-    for _ in range(args.warmup):
-        oracle_step(X, Y)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle_step(X, Y)
-    t = time.perf_counter() - t0
+    with pinned_to_one_core() as pin:
+        for _ in range(args.warmup):
+            oracle_step(X, Y)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle_step(X, Y)
+        t = time.perf_counter() - t0
     v = n_s * args.steps / t / 1e9
     sample = (f"c5 rows [0, 2^22) per step (X DYN_BP{{512}}, Y FOR_BP{{512}}): select X<2^16 -> DELTA_BP{{512}}, "
               f"project Y -> FOR_BP{{512}}, sum; oracle = plain C, one thread")
@@ -155,7 +189,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (counter-based splitmix64, SURVEY.md §8(d) d.2)",
             "config": {"workload": "c5 (BASELINE.json configs[4]) bounded CPU sample", "rows_per_step": n_s},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "pinned_cpu": pin.cpu, **host_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -166,13 +201,14 @@ def cpu_baseline_ours():
     """Oracle timed on a bounded sample of the same workload, on this host, one thread."""
     n_s = 1 << 24
     X, Y = oracle_sample(n_s)
-    t0 = time.perf_counter()
-    oracle_step(X, Y)
-    t = time.perf_counter() - t0
+    with pinned_to_one_core() as pin:
+        t0 = time.perf_counter()
+        oracle_step(X, Y)
+        t = time.perf_counter() - t0
     return {"value": n_s / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": "c5 rows [0, 2^24): select X<2^16 -> DELTA_BP{512}, project Y -> FOR_BP{512}, sum "
                       "(plain-C oracle, single thread, inputs pre-encoded)",
-            "seconds": t}
+            "seconds": t, "pinned_cpu": pin.cpu, **host_info()}
 
 
 def touched_gather_bytes(X, Y, start, pos_fmt):
@@ -321,11 +357,13 @@ def run_ours(args):
         kernels[k] = ent
     dom_name = max(prof.items(), key=lambda kv: kv[1][1])[0]
     dom = kernels[dom_name]
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        t = json.load(open(tpath)).get(dom_name)
-        traffic = t * (n / (1 << 28)) if (t is not None and json.load(open(tpath)).get("_per_2_28")) else t
+        tj = json.load(open(tpath))
+        if args.n_log2 == 32 and world == 1:  # captured at this workload (one GPU, 2^32 rows)
+            traffic = tj.get(dom_name)
+            traffic_src = tj.get("_about")
     step_ms = ms_total / args.steps
     chain_alg = x_bytes + bytes_pos + gather_bytes + 2 * bytes_yp
     value = n * args.steps / (ms_total * 1e-3) / 1e9
@@ -338,7 +376,7 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline_ours()
 
     if rank == 0:
@@ -352,9 +390,13 @@ def run_ours(args):
                        "X_bytes": x_bytes * (world if world > 1 else 1), "Y_bytes": y_bytes},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom.get("achieved_gbs"), "peak": peak,
                          "unit": "GB/s", "frac": dom.get("frac_of_peak"), "traffic": traffic,
+                         "frac_nominal": (dom.get("achieved_gbs") or 0) / NOMINAL_HBM_GBS,
+                         "nominal_peak": NOMINAL_HBM_GBS,
                          "alg_bytes_per_launch": dom.get("alg_bytes"), "avg_launch_ms": dom["avg_ms"],
-                         "peak_source": peak_src},
+                         "peak_source": peak_src, "traffic_source": traffic_src},
             "hbm_gbs_chain": chain_alg / (step_ms * 1e-3) / 1e9,
+            "chain_frac": chain_alg / (step_ms * 1e-3) / 1e9 / peak,
+            "chain_frac_nominal": chain_alg / (step_ms * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
             "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "parity": parity,
         }
@@ -430,10 +472,27 @@ def run_e2e(args, X, Y, start, world, dev, n):
             "note": "pinned host images -> ms_column_to_device -> select -> project -> sum -> 8 B result"}
 
 
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-run this script under
+    torch.distributed.run, one rank per GPU; rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     return run_ours(args)
 
 
