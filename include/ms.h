@@ -205,6 +205,54 @@ MS_API ms_status ms_agg_sum_grouped(const ms_ctx *ctx, const ms_column *gid, con
 MS_API ms_status ms_column_to_device(const ms_ctx *ctx, const ms_column *host_col, ms_column *out);
 MS_API ms_status ms_column_to_host(const ms_ctx *ctx, const ms_column *dev_col, ms_column *host_col);
 
+/* ---- plan-level operators (paper_2004_09350_b200/csrc/plan.cu) ---- */
+
+/* Exact footprints (ms_column_bytes) of `in` re-encoded in each candidate format,
+ * from ONE pass over the column (per block of block_size rows: max, min, largest
+ * in-block delta; the column max; the run count) — the compression-rate objective
+ * of the paper's cost-based format selection (DP2, P:66-68;
+ * S:384-394). sizes (HOST, MS_N_CANDIDATES uint64) in the order UNCOMPR,
+ * STATIC_BP (at its auto width), DYN_BP{block_size}, DELTA_BP{block_size},
+ * FOR_BP{block_size}, RLE. *best (may be NULL) = the smallest, ties broken by that
+ * order (simplest first). One synchronisation. */
+#define MS_N_CANDIDATES 6
+MS_API ms_status ms_format_sizes(const ms_ctx *ctx, const ms_column *in, uint32_t block_size, uint64_t *sizes,
+                                 ms_fmt *best);
+
+/* Sorted intersection / duplicate-free union of two strictly increasing position
+ * columns (conjunctive / disjunctive predicates of star-schema plans),
+ * out in out_fmt. Via a 1-bit mask over the inputs' common range and the select
+ * output encoders. MS_E_INVALID if an input is not strictly increasing (NotSorted).
+ * Two synchronisations (the inputs' ranges; the output size). */
+MS_API ms_status ms_intersect(const ms_ctx *ctx, const ms_column *a, const ms_column *b, ms_fmt out_fmt,
+                              ms_column *out);
+MS_API ms_status ms_merge(const ms_ctx *ctx, const ms_column *a, const ms_column *b, ms_fmt out_fmt,
+                          ms_column *out);
+
+/* Group ids: out_ids[i] = dense id of the (prev_ids[i], keys[i])
+ * combination in order of first occurrence (prev_ids may be NULL: keys alone);
+ * out_extents[g] = row of the first occurrence of group g (strictly increasing
+ * positions, in extents_fmt; UNCOMPR per S:309). max_groups: capacity hint of the
+ * hash table (0 = keys->n); more distinct groups than the table holds is
+ * MS_E_NOMEM. MS_E_INVALID if prev_ids->n != keys->n (LengthMismatch). */
+MS_API ms_status ms_group(const ms_ctx *ctx, const ms_column *keys, const ms_column *prev_ids, uint64_t max_groups,
+                          ms_fmt ids_fmt, ms_fmt extents_fmt, ms_column *out_ids, ms_column *out_extents);
+
+/* Equi-join: all pairs (i, j) with left[i] == right[j] as two
+ * position columns (positions into left, positions into right) in left_fmt /
+ * right_fmt. The build side is the smaller column (right on a tie); pairs are in
+ * probe-row order, then ascending build row. Hash table in device memory; the pair
+ * lists are materialised uncompressed once before their compression. */
+MS_API ms_status ms_join(const ms_ctx *ctx, const ms_column *left, const ms_column *right, ms_fmt left_fmt,
+                         ms_fmt right_fmt, ms_column *out_left, ms_column *out_right);
+
+/* Elementwise arithmetic mod 2^64 (star-schema measures such as
+ * price x discount): out[i] = a[i] op b[i], op = MS_ADD / MS_SUB / MS_MUL.
+ * MS_E_INVALID if a->n != b->n (LengthMismatch) or op is unknown. */
+enum { MS_ADD = 0, MS_SUB = 1, MS_MUL = 2 };
+MS_API ms_status ms_calc(const ms_ctx *ctx, int32_t op, const ms_column *a, const ms_column *b, ms_fmt out_fmt,
+                         ms_column *out);
+
 /* Reads and clears the library's sticky device error word for ctx->stream's
  * device (errors raised by the non-synchronising ops). Synchronises. */
 MS_API ms_status ms_check_errors(const ms_ctx *ctx);

@@ -2,6 +2,7 @@
 // (P:469, 477-479): validates descriptors, splits columns into main part and
 // remainder (by descriptor), sizes and allocates outputs, launches the
 // kernels and performs the op's single read-back synchronisation.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -498,6 +499,131 @@ ms_status compress_rle(const Ctx& ctx, const uint64_t* values, uint64_t n, ms_co
 // block may need 64 bits
 uint64_t full_cap(uint64_t n, uint32_t B) { return (n / B) * B; }
 
+// The output-side buffer layer of every position-producing operator (select,
+// intersect / merge, group extents): a mask of NS * 16 u32 words (1 bit per row,
+// rows >= n zero) plus per-segment info (count | 1-based last row << 16) ->
+// positions row_offset + row in out_fmt. Runs the segment scan, the
+// op's sizing read-back (with the producer's device error word err_in), the
+// encoders, and the final read-back of the widths.
+ms_status positions_from_mask(const Ctx& ctx, uint32_t* bits, uint32_t* seg_info, uint64_t NS, uint64_t n,
+                              uint64_t row_offset, ms_fmt out_fmt, const uint32_t* err_in, ms_column* out) {
+  const uint32_t G = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;  // output item size
+  const uint64_t items_max = (n + G - 1) / G + 1;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] 1 + max position
+  const uint64_t o_off = sc.add(8 * (NS + 1), false);  // the scan writes every entry
+  const uint64_t o_gs = sc.add(8 * (items_max + 1), false);
+  const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk1 = sc.add(8, true);
+  const bool pos_delta = out_fmt.format == MS_DELTA_BP && G <= 512;  // posdelta.cuh
+  // other formats with items <= 512: the slot encoder (MaskSource), no look-back
+  const bool pos_slots = !pos_delta && G <= 512 && out_fmt.format != MS_RLE;
+  const uint64_t o_st2 = sc.add(pos_delta || pos_slots ? 8 : 8 * (items_max + 1), true);  // look-back status
+  const uint64_t o_tk2 = sc.add(8, true);
+  const bool wscan = pos_delta || pos_slots;
+  const uint64_t o_wk = wscan ? sc.add(4 * (items_max + 1), false) : 0;
+  const uint64_t o_cwx = wscan ? sc.add(8 * (items_max + 2), false) : 0;
+  const uint64_t o_st3 = wscan ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
+  const uint64_t o_tk3 = wscan ? sc.add(8, true) : 0;
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  uint64_t* seg_off = sc.at<uint64_t>(o_off);
+  MS_TRY_CUDA(launch_seg_scan(seg_info, bits, NS, row_offset, G, seg_off, sc.at<uint64_t>(o_gs),
+                              sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1),
+                              ctx.s));
+  uint64_t h[4] = {0, 0, 0, 0};
+  if (NS) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], seg_off + NS, 8, cudaMemcpyDeviceToHost, ctx.s));
+  if (err_in) MS_TRY_CUDA(cudaMemcpyAsync(&h[3], err_in, 4, cudaMemcpyDeviceToHost, ctx.s));
+  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
+  MS_TRY(status_from_bits((uint32_t)h[0] | (uint32_t)h[3]));
+  const uint64_t n_out = NS ? h[2] : 0;
+  const uint64_t max_pos = h[1] ? h[1] - 1 : 0;
+  // size the output (n_out and the largest position are known now)
+  uint64_t cap = 0;
+  ms_fmt f = out_fmt;
+  switch (f.format) {
+    case MS_UNCOMPR: cap = n_out; break;
+    case MS_RLE: cap = 2 * n_out; break;
+    case MS_STATIC_BP: {
+      const uint32_t need = n_out ? (ebw_host(max_pos) ? ebw_host(max_pos) : 1) : 1;
+      if (f.bit_width == 0) f.bit_width = need;
+      else if (n_out && ebw_host(max_pos) > f.bit_width) return MS_E_WIDTH_OVERFLOW;
+      cap = words_for(n_out, f.bit_width);
+      break;
+    }
+    default: {
+      const uint32_t B = f.block_size;
+      const uint64_t nb = n_out / B;
+      uint64_t wsum = 64 * nb;
+      if (f.format == MS_DYN_BP) {
+        wsum = nb * ebw_host(max_pos);
+      } else if (nb) {  // sum_k ebw(span_k) <= nb (1 + log2(n / nb)) (Jensen; DESIGN.md)
+        const uint64_t q = (n + nb - 1) / nb;
+        const uint64_t lg = q > 1 ? 64 - __builtin_clzll(q - 1) : 0;
+        wsum = nb * (1 + lg);
+        if (wsum > 64 * nb) wsum = 64 * nb;
+      }
+      cap = wsum * (B / 64);
+    }
+  }
+  if (is_block(f.format) && 64 * (n_out / f.block_size) > 0xffffffffull) return MS_E_INVALID;
+  MS_TRY(alloc_column(ctx, out, f, n_out, cap, f.format == MS_RLE ? n_out : 0));
+  if (f.format == MS_UNCOMPR || f.format == MS_RLE || f.format == MS_STATIC_BP) out->payload_words = cap;
+  if (is_block(f.format)) {
+    cudaError_t e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
+    if (e != cudaSuccess) { release(ctx, out); return cuda_status(e); }
+  }
+  if (n_out) {
+    PosEnc pe{};
+    pe.format = f.format;
+    pe.w = f.bit_width;
+    pe.G = G;
+    pe.log2G = log2u(G);
+    pe.n_out = n_out;
+    pe.payload = out->payload;
+    pe.cw = out->cw;
+    pe.ref = out->ref;
+    pe.rem = out->rem;
+    // single-walk slots for DELTA_BP positions: every delta is < NS * 512 rows, so
+    // wcap = ebw(NS * 512 - 1) bits per code bound every block (B * wcap / 64 words per slot)
+    uint64_t* slots = nullptr;
+    uint32_t slot_words = 0;
+    if (pos_delta && f.format == MS_DELTA_BP) {
+      const uint32_t wcap = ebw_host(NS * kSegRows - 1);
+      slot_words = G / 64 * (wcap ? wcap : 1);
+      slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
+      if (!slots) { release(ctx, out); return MS_E_NOMEM; }
+    }
+    if (pos_slots && is_block(f.format) && n_out / G) {  // DYN_BP / FOR_BP positions: 64-bit slots
+      slot_words = G;  // G / 64 * 64
+      slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
+      if (!slots) { release(ctx, out); return MS_E_NOMEM; }
+    }
+    cudaError_t e =
+        pos_delta && f.format == MS_DELTA_BP
+            ? launch_positions_delta(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset,
+                                     sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
+                                     sc.at<uint32_t>(o_tk3), slots, slot_words, err, ctx.s)
+        : pos_slots
+            ? launch_positions_slots(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset, slots,
+                                     slot_words, sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx),
+                                     sc.at<uint64_t>(o_st3), sc.at<uint32_t>(o_tk3), err, ctx.s)
+            : launch_positions(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset,
+                               sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
+    ctx.free(slots);  // stream-ordered free: the copy kernel is queued before it
+    if (e != cudaSuccess) {
+      release(ctx, out);
+      return cuda_status(e);
+    }
+  }
+  const bool wmax_known = (pos_delta || pos_slots) && is_block(f.format) && n_out / G;
+  ms_status st = finish_output(ctx, out, err, wmax_known ? sc.at<uint64_t>(o_cwx) + n_out / G + 1 : nullptr);
+  if (st == MS_OK) st = maybe_shrink(ctx, out);
+  if (st != MS_OK) release(ctx, out);
+  return st;
+}
+
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -696,128 +822,21 @@ ms_status ms_select(const ms_ctx* ctx_, const ms_column* in, const ms_pred* pred
   const uint64_t n = in->n;
   const uint64_t NS = (n + kSegRows - 1) / kSegRows;  // 512-row segments
   const uint64_t n_words = NS * kSegWords;
-  const uint32_t G = is_block(out_fmt.format) ? out_fmt.block_size : (uint32_t)kSegRows;  // output item size
-  const uint64_t items_max = (n + G - 1) / G + 1;
   Scratch sc(ctx);
-  const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] 1 + max position
+  const uint64_t o_meta = sc.add(64, true);  // [0] err
   const uint64_t o_bits = sc.add(4 * n_words, false);
   const uint64_t o_seg = sc.add(4 * (NS + 1), false);
   const uint64_t o_list = sc.add(4 * ((NS * kSegRows + kChunk - 1) / kChunk + 2), false);  // pruning work list
-  const uint64_t o_off = sc.add(8 * (NS + 1), false);  // the scan writes every entry
-  const uint64_t o_gs = sc.add(8 * (items_max + 1), false);
-  const uint64_t o_st1 = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
-  const uint64_t o_tk1 = sc.add(8, true);
-  const bool pos_delta = out_fmt.format == MS_DELTA_BP && G <= 512;  // posdelta.cuh
-  // other formats with items <= 512: the slot encoder (MaskSource), no look-back
-  const bool pos_slots = !pos_delta && G <= 512 && out_fmt.format != MS_RLE;
-  const uint64_t o_st2 = sc.add(pos_delta || pos_slots ? 8 : 8 * (items_max + 1), true);  // look-back status
-  const uint64_t o_tk2 = sc.add(8, true);
-  const bool wscan = pos_delta || pos_slots;
-  const uint64_t o_wk = wscan ? sc.add(4 * (items_max + 1), false) : 0;
-  const uint64_t o_cwx = wscan ? sc.add(8 * (items_max + 2), false) : 0;
-  const uint64_t o_st3 = wscan ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
-  const uint64_t o_tk3 = wscan ? sc.add(8, true) : 0;
   RlePrep rp;
   plan_rle(sc, in, rp);
   if (!sc.commit()) return MS_E_NOMEM;
   uint32_t* err = sc.at<uint32_t>(o_meta);
   ColView src = view_of(in);
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
-  uint64_t* seg_off = sc.at<uint64_t>(o_off);
   MS_TRY_CUDA(launch_select(src, ps, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, sc.at<uint32_t>(o_list),
                             err, ctx.s));
-  MS_TRY_CUDA(launch_seg_scan(sc.at<uint32_t>(o_seg), sc.at<uint32_t>(o_bits), NS, row_offset, G, seg_off,
-                              sc.at<uint64_t>(o_gs), sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1),
-                              sc.at<uint32_t>(o_tk1), ctx.s));
-  uint64_t h[3] = {0, 0, 0};
-  if (NS) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], seg_off + NS, 8, cudaMemcpyDeviceToHost, ctx.s));
-  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
-  MS_TRY(status_from_bits((uint32_t)h[0]));
-  const uint64_t n_out = NS ? h[2] : 0;
-  const uint64_t max_pos = h[1] ? h[1] - 1 : 0;
-  // size the output (n_out and the largest position are known now)
-  uint64_t cap = 0;
-  ms_fmt f = out_fmt;
-  switch (f.format) {
-    case MS_UNCOMPR: cap = n_out; break;
-    case MS_RLE: cap = 2 * n_out; break;
-    case MS_STATIC_BP: {
-      const uint32_t need = n_out ? (ebw_host(max_pos) ? ebw_host(max_pos) : 1) : 1;
-      if (f.bit_width == 0) f.bit_width = need;
-      else if (n_out && ebw_host(max_pos) > f.bit_width) return MS_E_WIDTH_OVERFLOW;
-      cap = words_for(n_out, f.bit_width);
-      break;
-    }
-    default: {
-      const uint32_t B = f.block_size;
-      const uint64_t nb = n_out / B;
-      uint64_t wsum = 64 * nb;
-      if (f.format == MS_DYN_BP) {
-        wsum = nb * ebw_host(max_pos);
-      } else if (nb) {  // sum_k ebw(span_k) <= nb (1 + log2(n / nb)) (Jensen; DESIGN.md)
-        const uint64_t q = (n + nb - 1) / nb;
-        const uint64_t lg = q > 1 ? 64 - __builtin_clzll(q - 1) : 0;
-        wsum = nb * (1 + lg);
-        if (wsum > 64 * nb) wsum = 64 * nb;
-      }
-      cap = wsum * (B / 64);
-    }
-  }
-  if (is_block(f.format) && 64 * (n_out / f.block_size) > 0xffffffffull) return MS_E_INVALID;
-  MS_TRY(alloc_column(ctx, out, f, n_out, cap, f.format == MS_RLE ? n_out : 0));
-  if (f.format == MS_UNCOMPR || f.format == MS_RLE || f.format == MS_STATIC_BP) out->payload_words = cap;
-  if (is_block(f.format)) {
-    cudaError_t e = cudaMemsetAsync(out->cw, 0, 4, ctx.s);
-    if (e != cudaSuccess) { release(ctx, out); return cuda_status(e); }
-  }
-  if (n_out) {
-    PosEnc pe{};
-    pe.format = f.format;
-    pe.w = f.bit_width;
-    pe.G = G;
-    pe.log2G = log2u(G);
-    pe.n_out = n_out;
-    pe.payload = out->payload;
-    pe.cw = out->cw;
-    pe.ref = out->ref;
-    pe.rem = out->rem;
-    // single-walk slots for DELTA_BP positions: every delta is < NS * 512 rows, so
-    // wcap = ebw(NS * 512 - 1) bits per code bound every block (B * wcap / 64 words per slot)
-    uint64_t* slots = nullptr;
-    uint32_t slot_words = 0;
-    if (pos_delta && f.format == MS_DELTA_BP) {
-      const uint32_t wcap = ebw_host(NS * kSegRows - 1);
-      slot_words = G / 64 * (wcap ? wcap : 1);
-      slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
-      if (!slots) { release(ctx, out); return MS_E_NOMEM; }
-    }
-    if (pos_slots && is_block(f.format) && n_out / G) {  // DYN_BP / FOR_BP positions: 64-bit slots
-      slot_words = G;  // G / 64 * 64
-      slots = (uint64_t*)ctx.alloc(8 * (n_out / G) * (uint64_t)slot_words);
-      if (!slots) { release(ctx, out); return MS_E_NOMEM; }
-    }
-    cudaError_t e =
-        pos_delta && f.format == MS_DELTA_BP
-            ? launch_positions_delta(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
-                                     sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
-                                     sc.at<uint32_t>(o_tk3), slots, slot_words, err, ctx.s)
-        : pos_slots
-            ? launch_positions_slots(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset, slots,
-                                     slot_words, sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx),
-                                     sc.at<uint64_t>(o_st3), sc.at<uint32_t>(o_tk3), err, ctx.s)
-            : launch_positions(pe, sc.at<uint32_t>(o_bits), NS, sc.at<uint64_t>(o_gs), row_offset,
-                               sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2), err, ctx.s);
-    ctx.free(slots);  // stream-ordered free: the copy kernel is queued before it
-    if (e != cudaSuccess) {
-      release(ctx, out);
-      return cuda_status(e);
-    }
-  }
-  const bool wmax_known = (pos_delta || pos_slots) && is_block(f.format) && n_out / G;
-  ms_status st = finish_output(ctx, out, err, wmax_known ? sc.at<uint64_t>(o_cwx) + n_out / G + 1 : nullptr);
-  if (st == MS_OK) st = maybe_shrink(ctx, out);
-  if (st != MS_OK) release(ctx, out);
-  return st;
+  return positions_from_mask(ctx, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, n, row_offset, out_fmt, err,
+                             out);
 }
 
 ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column* positions, uint64_t row_offset,
@@ -1039,6 +1058,279 @@ ms_status ms_column_to_host(const ms_ctx* ctx_, const ms_column* d, ms_column* h
   h->alloc = nullptr;
   h->alloc_bytes = 0;
   return MS_OK;
+}
+
+// ------------------------------------------------------------ plan-level operators (plan.cu)
+ms_status ms_format_sizes(const ms_ctx* ctx_, const ms_column* in, uint32_t block_size, uint64_t* sizes,
+                          ms_fmt* best) {
+  MS_TRY(check_col(in));
+  if (!sizes || !valid_B(block_size)) return MS_E_INVALID;
+  Ctx ctx(ctx_);
+  const uint64_t n = in->n, B = block_size, nb = n / B, nrem = n % B;
+  const uint64_t T = (n + kChunk - 1) / kChunk;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);   // [0] err
+  const uint64_t o_acc = sc.add(64, true);    // max, sum w DYN, sum w DELTA, sum w FOR, runs
+  const uint64_t o_fl = sc.add(16 * (T + 1), false);
+  RlePrep rp;
+  plan_rle(sc, in, rp);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView v = view_of(in);
+  MS_TRY_CUDA(run_rle(sc, in, rp, v, err));
+  MS_TRY_CUDA(launch_profile(v, block_size, sc.at<unsigned long long>(o_acc), sc.at<uint64_t>(o_fl), ctx.s));
+  uint64_t h[8] = {0};
+  MS_TRY_CUDA(cudaMemcpyAsync(h + 1, sc.at<uint64_t>(o_acc), 40, cudaMemcpyDeviceToHost, ctx.s));
+  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 1));  // the op's one sync
+  MS_TRY(status_from_bits((uint32_t)h[0]));
+  const uint64_t mx = h[1], hdr = 4 * (nb + 1) + 8 * nrem;
+  const uint32_t w = ebw_host(mx) ? ebw_host(mx) : 1;
+  sizes[0] = 8 * n;                                   // UNCOMPR
+  sizes[1] = 8 * words_for(n, w);                     // STATIC_BP at its auto width
+  sizes[2] = 8 * (h[2] * (B / 64)) + hdr;             // DYN_BP{B}
+  sizes[3] = 8 * (h[3] * (B / 64)) + hdr + 8 * nb;    // DELTA_BP{B}
+  sizes[4] = 8 * (h[4] * (B / 64)) + hdr + 8 * nb;    // FOR_BP{B}
+  sizes[5] = n ? 16 * h[5] : 0;                       // RLE
+  if (best) {
+    int k = 0;
+    for (int i = 1; i < MS_N_CANDIDATES; ++i)
+      if (sizes[i] < sizes[k]) k = i;  // ties: the earlier (simpler) format
+    const int32_t order[MS_N_CANDIDATES] = {MS_UNCOMPR, MS_STATIC_BP, MS_DYN_BP, MS_DELTA_BP, MS_FOR_BP, MS_RLE};
+    *best = ms_fmt{order[k], order[k] == MS_STATIC_BP ? w : 0u, is_block(order[k]) ? block_size : 0u, 0u};
+  }
+  return MS_OK;
+}
+
+// intersect (op 0) / merge (op 1) of two strictly increasing position columns via a
+// bit mask over the positions' common range, then the select output encoders
+static ms_status set_op(const ms_ctx* ctx_, const ms_column* a, const ms_column* b, int op, ms_fmt out_fmt,
+                        ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(a));
+  MS_TRY(check_col(b));
+  MS_TRY(check_fmt(out_fmt));
+  Ctx ctx(ctx_);
+  Scratch s1(ctx);
+  const uint64_t o_meta = s1.add(64, true);
+  const uint64_t o_ends = s1.add(32, false);
+  RlePrep ra, rb;
+  plan_rle(s1, a, ra);
+  plan_rle(s1, b, rb);
+  if (!s1.commit()) return MS_E_NOMEM;
+  uint32_t* err = s1.at<uint32_t>(o_meta);
+  ColView va = view_of(a), vb = view_of(b);
+  MS_TRY_CUDA(run_rle(s1, a, ra, va, err));
+  MS_TRY_CUDA(run_rle(s1, b, rb, vb, err));
+  MS_TRY_CUDA(launch_ends(va, vb, s1.at<uint64_t>(o_ends), ctx.s));
+  uint64_t e[4];
+  MS_TRY(readback(ctx, s1.at<uint64_t>(o_ends), e, 4));  // sizing sync: the ranges
+  uint64_t lo = 0, hi = 0;
+  bool empty = false;
+  if (op == 0) {
+    empty = !a->n || !b->n || std::max(e[0], e[2]) > std::min(e[1], e[3]);
+    lo = std::max(e[0], e[2]);
+    hi = std::min(e[1], e[3]);
+  } else if (!a->n && !b->n) {
+    empty = true;
+  } else {
+    lo = !a->n ? e[2] : (!b->n ? e[0] : std::min(e[0], e[2]));
+    hi = !a->n ? e[3] : (!b->n ? e[1] : std::max(e[1], e[3]));
+  }
+  const uint64_t nbits = empty ? 0 : hi - lo + 1;
+  if (!empty && nbits == 0) return MS_E_INVALID;  // the whole 2^64 range
+  const uint64_t NS = (nbits + kSegRows - 1) / kSegRows, n_words = NS * kSegWords;
+  Scratch s2(ctx);
+  const uint64_t o_ba = s2.add(4 * n_words, true);
+  const uint64_t o_bb = s2.add(4 * n_words, true);
+  const uint64_t o_fa = s2.add(16 * ((a->n + kChunk - 1) / kChunk + 1), false);
+  const uint64_t o_fb = s2.add(16 * ((b->n + kChunk - 1) / kChunk + 1), false);
+  const uint64_t o_seg = s2.add(4 * (NS + 1), false);
+  if (!s2.commit()) return MS_E_NOMEM;
+  uint32_t* ba = s2.at<uint32_t>(o_ba);
+  if (!empty) {
+    MS_TRY_CUDA(launch_pos_bitmap(va, lo, nbits, ba, s2.at<uint64_t>(o_fa), err, ctx.s));
+    MS_TRY_CUDA(launch_pos_bitmap(vb, lo, nbits, s2.at<uint32_t>(o_bb), s2.at<uint64_t>(o_fb), err, ctx.s));
+    MS_TRY_CUDA(launch_bits_combine(ba, s2.at<uint32_t>(o_bb), n_words, op, ctx.s));
+    MS_TRY_CUDA(launch_seg_info(ba, NS, s2.at<uint32_t>(o_seg), ctx.s));
+  }
+  return positions_from_mask(ctx, ba, s2.at<uint32_t>(o_seg), NS, nbits, lo, out_fmt, err, out);
+}
+
+ms_status ms_intersect(const ms_ctx* ctx, const ms_column* a, const ms_column* b, ms_fmt out_fmt, ms_column* out) {
+  return set_op(ctx, a, b, 0, out_fmt, out);
+}
+ms_status ms_merge(const ms_ctx* ctx, const ms_column* a, const ms_column* b, ms_fmt out_fmt, ms_column* out) {
+  return set_op(ctx, a, b, 1, out_fmt, out);
+}
+
+static uint64_t pow2_at_least(uint64_t x) {
+  uint64_t c = 1024;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+ms_status ms_group(const ms_ctx* ctx_, const ms_column* keys, const ms_column* prev_ids, uint64_t max_groups,
+                   ms_fmt ids_fmt, ms_fmt extents_fmt, ms_column* out_ids, ms_column* out_extents) {
+  if (!out_ids || !out_extents) return MS_E_INVALID;
+  std::memset(out_ids, 0, sizeof(*out_ids));
+  std::memset(out_extents, 0, sizeof(*out_extents));
+  MS_TRY(check_col(keys));
+  if (prev_ids) MS_TRY(check_col(prev_ids));
+  MS_TRY(check_fmt(ids_fmt));
+  MS_TRY(check_fmt(extents_fmt));
+  if (prev_ids && prev_ids->n != keys->n) return MS_E_INVALID;  // LengthMismatch
+  Ctx ctx(ctx_);
+  const uint64_t n = keys->n;
+  const uint64_t groups = max_groups && max_groups < n ? max_groups : n;
+  const uint64_t cap = pow2_at_least(2 * (groups ? groups : 1));
+  const uint64_t NS = (n + kSegRows - 1) / kSegRows, n_words = NS * kSegWords;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_state = sc.add(4 * cap, true);
+  const uint64_t o_key = sc.add(8 * cap, false);
+  const uint64_t o_key2 = sc.add(prev_ids ? 8 * cap : 8, false);
+  const uint64_t o_first = sc.add(8 * cap, false);
+  const uint64_t o_bits = sc.add(4 * n_words, true);
+  const uint64_t o_cnt = sc.add(4 * (NS + 1), false);
+  const uint64_t o_off = sc.add(8 * (NS + 2), false);
+  const uint64_t o_st = sc.add(8 * ((NS + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk = sc.add(8, true);
+  const uint64_t o_seg = sc.add(4 * (NS + 1), false);
+  const uint64_t o_ids = sc.add(8 * n, false);
+  RlePrep rk, rpv;
+  plan_rle(sc, keys, rk);
+  plan_rle(sc, prev_ids, rpv);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView vk = view_of(keys), vp{};
+  MS_TRY_CUDA(run_rle(sc, keys, rk, vk, err));
+  if (prev_ids) {
+    vp = view_of(prev_ids);
+    MS_TRY_CUDA(run_rle(sc, prev_ids, rpv, vp, err));
+  }
+  uint32_t* state = sc.at<uint32_t>(o_state);
+  uint64_t* key = sc.at<uint64_t>(o_key);
+  uint64_t* key2 = prev_ids ? sc.at<uint64_t>(o_key2) : nullptr;
+  auto* first = sc.at<unsigned long long>(o_first);
+  uint32_t* bits = sc.at<uint32_t>(o_bits);
+  MS_TRY_CUDA(cudaMemsetAsync(first, 0xff, 8 * cap, ctx.s));
+  if (n) {
+    MS_TRY_CUDA(launch_group(vk, vp, state, key, key2, cap, first, bits, err, ctx.s));
+    MS_TRY_CUDA(launch_seg_count(bits, NS, sc.at<uint32_t>(o_cnt), ctx.s));
+    MS_TRY_CUDA(launch_count_scan(sc.at<uint32_t>(o_cnt), NS, sc.at<uint64_t>(o_off), sc.at<uint64_t>(o_st),
+                                  sc.at<uint32_t>(o_tk), ctx.s));
+    MS_TRY_CUDA(launch_group_ids(vk, vp, state, key, key2, cap, first, bits, sc.at<uint64_t>(o_off),
+                                 sc.at<uint64_t>(o_ids), err, ctx.s));
+    MS_TRY_CUDA(launch_seg_info(bits, NS, sc.at<uint32_t>(o_seg), ctx.s));
+  }
+  // extents: the first row of every group = the set bits of the mask (sync, errors read here)
+  MS_TRY(positions_from_mask(ctx, bits, sc.at<uint32_t>(o_seg), NS, n, 0, extents_fmt, err, out_extents));
+  const ms_status st = ms_compress(ctx_, sc.at<uint64_t>(o_ids), n, ids_fmt, out_ids);
+  if (st != MS_OK) release(ctx, out_extents);
+  return st;
+}
+
+ms_status ms_join(const ms_ctx* ctx_, const ms_column* left, const ms_column* right, ms_fmt left_fmt,
+                  ms_fmt right_fmt, ms_column* out_left, ms_column* out_right) {
+  if (!out_left || !out_right) return MS_E_INVALID;
+  std::memset(out_left, 0, sizeof(*out_left));
+  std::memset(out_right, 0, sizeof(*out_right));
+  MS_TRY(check_col(left));
+  MS_TRY(check_col(right));
+  MS_TRY(check_fmt(left_fmt));
+  MS_TRY(check_fmt(right_fmt));
+  Ctx ctx(ctx_);
+  const bool build_right = right->n <= left->n;  // build side = the smaller column
+  const ms_column* build = build_right ? right : left;
+  const ms_column* probe = build_right ? left : right;
+  const uint64_t cap = pow2_at_least(2 * (build->n ? build->n : 1));
+  const uint64_t T = (probe->n + kChunk - 1) / kChunk;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_state = sc.add(4 * cap, true);
+  const uint64_t o_key = sc.add(8 * cap, false);
+  const uint64_t o_cnt = sc.add(4 * cap, true);
+  const uint64_t o_off = sc.add(8 * (cap + 2), false);
+  const uint64_t o_fill = sc.add(4 * cap, true);
+  const uint64_t o_rows = sc.add(8 * build->n, false);
+  const uint64_t o_st1 = sc.add(8 * ((cap + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk1 = sc.add(8, true);
+  const uint64_t o_tc = sc.add(4 * (T + 1), false);
+  const uint64_t o_toff = sc.add(8 * (T + 2), false);
+  const uint64_t o_st2 = sc.add(8 * ((T + kChunk - 1) / kChunk + 1), true);
+  const uint64_t o_tk2 = sc.add(8, true);
+  RlePrep rb, rp;
+  plan_rle(sc, build, rb);
+  plan_rle(sc, probe, rp);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView vb = view_of(build), vpr = view_of(probe);
+  MS_TRY_CUDA(run_rle(sc, build, rb, vb, err));
+  MS_TRY_CUDA(run_rle(sc, probe, rp, vpr, err));
+  uint32_t* state = sc.at<uint32_t>(o_state);
+  uint64_t* key = sc.at<uint64_t>(o_key);
+  uint32_t* cnt = sc.at<uint32_t>(o_cnt);
+  uint64_t* off = sc.at<uint64_t>(o_off);
+  uint64_t* toff = sc.at<uint64_t>(o_toff);
+  uint64_t total = 0;
+  if (build->n && probe->n) {
+    MS_TRY_CUDA(launch_join_build(vb, state, key, cap, cnt, err, ctx.s));
+    MS_TRY_CUDA(launch_count_scan(cnt, cap, off, sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1), ctx.s));
+    MS_TRY_CUDA(launch_join_place(vb, state, key, cap, cnt, off, sc.at<uint32_t>(o_fill), sc.at<uint64_t>(o_rows),
+                                  err, ctx.s));
+    MS_TRY_CUDA(launch_join_probe(vpr, state, key, cap, cnt, off, sc.at<uint64_t>(o_rows), sc.at<uint32_t>(o_tc),
+                                  toff, nullptr, nullptr, false, err, ctx.s));
+    MS_TRY_CUDA(launch_count_scan(sc.at<uint32_t>(o_tc), T, toff, sc.at<uint64_t>(o_st2), sc.at<uint32_t>(o_tk2),
+                                  ctx.s));
+    uint64_t h[2] = {0, 0};
+    MS_TRY_CUDA(cudaMemcpyAsync(&h[1], toff + T, 8, cudaMemcpyDeviceToHost, ctx.s));
+    MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 1));  // sizing sync: the number of pairs
+    MS_TRY(status_from_bits((uint32_t)h[0]));
+    total = h[1];
+  }
+  uint64_t* pairs = (uint64_t*)ctx.alloc(16 * (total ? total : 1));
+  if (!pairs) return MS_E_NOMEM;
+  uint64_t *pp = pairs, *pb = pairs + total;
+  ms_status st = MS_OK;
+  if (total) st = cuda_status(launch_join_probe(vpr, state, key, cap, cnt, off, sc.at<uint64_t>(o_rows),
+                                                sc.at<uint32_t>(o_tc), toff, pp, pb, true, err, ctx.s));
+  if (st == MS_OK) st = ms_compress(ctx_, build_right ? pp : pb, total, left_fmt, out_left);
+  if (st == MS_OK) {
+    st = ms_compress(ctx_, build_right ? pb : pp, total, right_fmt, out_right);
+    if (st != MS_OK) release(ctx, out_left);
+  }
+  ctx.free(pairs);
+  return st;
+}
+
+ms_status ms_calc(const ms_ctx* ctx_, int32_t op, const ms_column* a, const ms_column* b, ms_fmt out_fmt,
+                  ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(a));
+  MS_TRY(check_col(b));
+  MS_TRY(check_fmt(out_fmt));
+  if (a->n != b->n) return MS_E_INVALID;  // LengthMismatch
+  if (op != MS_ADD && op != MS_SUB && op != MS_MUL) return MS_E_INVALID;
+  Ctx ctx(ctx_);
+  const uint64_t n = a->n;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_out = sc.add(8 * n, false);
+  RlePrep ra, rb;
+  plan_rle(sc, a, ra);
+  plan_rle(sc, b, rb);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  ColView va = view_of(a), vb = view_of(b);
+  MS_TRY_CUDA(run_rle(sc, a, ra, va, err));
+  MS_TRY_CUDA(run_rle(sc, b, rb, vb, err));
+  MS_TRY_CUDA(launch_calc(va, vb, op, sc.at<uint64_t>(o_out), ctx.s));
+  uint64_t h = 0;
+  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), &h, 1));
+  MS_TRY(status_from_bits((uint32_t)h));
+  return ms_compress(ctx_, sc.at<uint64_t>(o_out), n, out_fmt, out);
 }
 
 ms_status ms_check_errors(const ms_ctx* ctx_) {

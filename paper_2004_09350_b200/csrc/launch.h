@@ -120,6 +120,33 @@ cudaError_t launch_sum_at(const ColView& data, const ColView& pos, uint64_t row_
 cudaError_t launch_sum_grouped(const ColView& gid, const ColView& vals, uint64_t n_groups,
                                unsigned long long* sums, uint32_t* err, cudaStream_t s);
 
+// per 512-row segment of a mask: count | (1-based last set row << 16) (select.cu)
+cudaError_t launch_seg_info(const uint32_t* bits, uint64_t NS, uint32_t* seg_info, cudaStream_t s);
+
+// plan-level operators (plan.cu)
+// format profile: acc (5 u64, zeroed) = [max, sum ebw(max_b), sum ebw(maxdelta_b), sum ebw(max_b - min_b),
+// runs]; first_last: 2 u64 per 2048-row tile (scratch)
+cudaError_t launch_profile(const ColView& c, uint32_t B, unsigned long long* acc, uint64_t* first_last,
+                           cudaStream_t s);
+cudaError_t launch_seg_count(const uint32_t* bits, uint64_t NS, uint32_t* cnt, cudaStream_t s);
+cudaError_t launch_ends(const ColView& a, const ColView& b, uint64_t* out, cudaStream_t s);  // out: a0 a1 b0 b1
+cudaError_t launch_pos_bitmap(const ColView& c, uint64_t base, uint64_t nbits, uint32_t* bits, uint64_t* first_last,
+                              uint32_t* err, cudaStream_t s);
+cudaError_t launch_bits_combine(uint32_t* a, const uint32_t* b, uint64_t n_words, int op, cudaStream_t s);
+cudaError_t launch_group(const ColView& keys, const ColView& prev, uint32_t* state, uint64_t* key, uint64_t* key2,
+                         uint64_t cap, unsigned long long* first, uint32_t* bits, uint32_t* err, cudaStream_t s);
+cudaError_t launch_group_ids(const ColView& keys, const ColView& prev, uint32_t* state, uint64_t* key, uint64_t* key2,
+                             uint64_t cap, const unsigned long long* first, const uint32_t* bits,
+                             const uint64_t* seg_off, uint64_t* ids, uint32_t* err, cudaStream_t s);
+cudaError_t launch_join_build(const ColView& build, uint32_t* state, uint64_t* key, uint64_t cap, uint32_t* cnt,
+                              uint32_t* err, cudaStream_t s);
+cudaError_t launch_join_place(const ColView& build, uint32_t* state, uint64_t* key, uint64_t cap, const uint32_t* cnt,
+                              const uint64_t* off, uint32_t* fill, uint64_t* rows, uint32_t* err, cudaStream_t s);
+cudaError_t launch_join_probe(const ColView& probe, uint32_t* state, uint64_t* key, uint64_t cap, const uint32_t* cnt,
+                              const uint64_t* off, const uint64_t* rows, uint32_t* tile_cnt, const uint64_t* tile_off,
+                              uint64_t* out_probe, uint64_t* out_build, bool write, uint32_t* err, cudaStream_t s);
+cudaError_t launch_calc(const ColView& a, const ColView& b, int op, uint64_t* out, cudaStream_t s);
+
 int num_sms();
 // largest block width max(cw[b+1] - cw[b]) into *out (zero-initialised)
 cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cudaStream_t s);

@@ -219,6 +219,15 @@ __global__ void __launch_bounds__(256) seg_info_kernel(const uint32_t* bits, uin
   }
 }
 
+cudaError_t launch_seg_info(const uint32_t* bits, uint64_t NS, uint32_t* seg_info, cudaStream_t s) {
+  if (!NS) return cudaSuccess;
+  uint64_t g2 = (NS + 15) / 16;
+  if (g2 > (uint64_t)num_sms() * 16) g2 = num_sms() * 16;
+  ProfScope prof_("seg_info", s);
+  seg_info_kernel<<<(int)g2, 256, 0, s>>>(bits, NS, seg_info);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, uint32_t* seg_info, uint64_t NS,
                           uint32_t* tile_list, uint32_t* err, cudaStream_t s) {
   if (NS == 0) return cudaSuccess;

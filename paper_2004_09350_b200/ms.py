@@ -102,6 +102,12 @@ def _load():
         "ms_column_to_device": ([P(_Ctx), C, C], st),
         "ms_column_to_host": ([P(_Ctx), C, C], st),
         "ms_check_errors": ([P(_Ctx)], st),
+        "ms_format_sizes": ([P(_Ctx), C, ctypes.c_uint32, vp, P(_Fmt)], st),
+        "ms_intersect": ([P(_Ctx), C, C, _Fmt, C], st),
+        "ms_merge": ([P(_Ctx), C, C, _Fmt, C], st),
+        "ms_group": ([P(_Ctx), C, C, u64, _Fmt, _Fmt, C, C], st),
+        "ms_join": ([P(_Ctx), C, C, _Fmt, _Fmt, C, C], st),
+        "ms_calc": ([P(_Ctx), ctypes.c_int32, C, C, _Fmt, C], st),
         "ms_column_release": ([P(_Ctx), C], None),
         "ms_column_bytes": ([C], u64),
         "ms_status_str": ([ctypes.c_int], ctypes.c_char_p),
@@ -375,6 +381,75 @@ def agg_sum_grouped(gid: Column, vals: Column, n_groups: int, out: Optional[torc
     if check:
         check_errors(stream)
     return out
+
+
+# ------------------------------------------------------------ plan-level operators
+CANDIDATES = ("UNCOMPR", "STATIC_BP", "DYN_BP", "DELTA_BP", "FOR_BP", "RLE")  # ms_format_sizes order
+ADD, SUB, MUL = 0, 1, 2
+
+
+def format_sizes(col: Column, block_size: int = 512, stream=None) -> tuple[dict, Fmt]:
+    """ms_format_sizes: exact footprint of col in every candidate format (one pass,
+    one sync) and the smallest (ties: the simpler format). Returns ({name: bytes}, Fmt)."""
+    sizes = np.zeros(6, np.uint64)
+    best = _Fmt()
+    _uses(stream, col)
+    _check(_lib.ms_format_sizes(ctypes.byref(_ctx(stream)), ctypes.byref(col._c), block_size, sizes.ctypes.data,
+                                ctypes.byref(best)), "ms_format_sizes")
+    return dict(zip(CANDIDATES, (int(x) for x in sizes))), Fmt(best.format, best.bit_width, best.block_size)
+
+
+def choose_format(col: Column, block_size: int = 512, stream=None) -> Fmt:
+    return format_sizes(col, block_size, stream)[1]
+
+
+def _binary_pos_op(fn, name, a: Column, b: Column, out_fmt, stream):
+    out = _Column()
+    s = _uses(stream, a, b)
+    _check(fn(ctypes.byref(_ctx(stream)), ctypes.byref(a._c), ctypes.byref(b._c), _fmt(out_fmt), ctypes.byref(out)),
+           name)
+    return Column(out, stream=s)
+
+
+def intersect(a: Column, b: Column, out_fmt=None, stream=None) -> Column:
+    """ms_intersect: sorted intersection of two strictly increasing position columns."""
+    return _binary_pos_op(_lib.ms_intersect, "ms_intersect", a, b, out_fmt or delta_bp(512), stream)
+
+
+def merge(a: Column, b: Column, out_fmt=None, stream=None) -> Column:
+    """ms_merge: sorted duplicate-free union of two strictly increasing position columns."""
+    return _binary_pos_op(_lib.ms_merge, "ms_merge", a, b, out_fmt or delta_bp(512), stream)
+
+
+def group(keys: Column, prev_ids: Optional[Column] = None, max_groups: int = 0, ids_fmt=None, extents_fmt=None,
+          stream=None) -> tuple[Column, Column]:
+    """ms_group -> (group ids, extents)."""
+    ids, ext = _Column(), _Column()
+    s = _uses(stream, keys, prev_ids)
+    _check(_lib.ms_group(ctypes.byref(_ctx(stream)), ctypes.byref(keys._c),
+                         ctypes.byref(prev_ids._c) if prev_ids is not None else None, max_groups,
+                         _fmt(ids_fmt or uncompr()), _fmt(extents_fmt or uncompr()), ctypes.byref(ids),
+                         ctypes.byref(ext)), "ms_group")
+    return Column(ids, stream=s), Column(ext, stream=s)
+
+
+def join(left: Column, right: Column, left_fmt=None, right_fmt=None, stream=None) -> tuple[Column, Column]:
+    """ms_join -> (positions into left, positions into right)."""
+    lo, ro = _Column(), _Column()
+    s = _uses(stream, left, right)
+    _check(_lib.ms_join(ctypes.byref(_ctx(stream)), ctypes.byref(left._c), ctypes.byref(right._c),
+                        _fmt(left_fmt or uncompr()), _fmt(right_fmt or uncompr()), ctypes.byref(lo),
+                        ctypes.byref(ro)), "ms_join")
+    return Column(lo, stream=s), Column(ro, stream=s)
+
+
+def calc(op: int, a: Column, b: Column, out_fmt=None, stream=None) -> Column:
+    """ms_calc: elementwise ADD / SUB / MUL mod 2^64."""
+    out = _Column()
+    s = _uses(stream, a, b)
+    _check(_lib.ms_calc(ctypes.byref(_ctx(stream)), op, ctypes.byref(a._c), ctypes.byref(b._c),
+                        _fmt(out_fmt or uncompr()), ctypes.byref(out)), "ms_calc")
+    return Column(out, stream=s)
 
 
 def check_errors(stream=None):
