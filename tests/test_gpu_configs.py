@@ -237,6 +237,32 @@ def test_c4_reduced():
     assert np.array_equal(g["g2"], O.agg_sum_grouped(gid, m2p, 1000))
 
 
+def test_c4_formats_chosen_at_run_time():
+    """BJ.c4 with every intermediate re-encoded in the format the GPU's exact-size
+    profile chooses (ms_format_sizes: the compression-rate objective of P:722-735,
+    ties by S:392's order): each choice equals the oracle's choice on the same
+    values, and the chain's grouped sums are unchanged (format transparency)."""
+    ms = get_ms()
+    n = 1 << 22
+    from oracle import plan_ops as P
+    g = c4_chain(ms, n)
+    chosen = {}
+    for name in ("pos1", "k1p", "idx", "pos2", "m1p", "m2p", "k3p", "gid"):
+        c = g[name]
+        sizes, best = ms.format_sizes(c, 512)
+        vals = ms.to_u64_numpy(ms.decompress(c))
+        assert best.format == P.choose_format(vals, 512), name
+        assert [sizes[k] for k in ms.CANDIDATES] == P.format_sizes(vals, 512), name
+        m = ms.morph(c, best)
+        assert m.footprint() == min(sizes.values()), name
+        assert np.array_equal(ms.to_u64_numpy(ms.decompress(m)), vals), name
+        chosen[name] = (best, m)
+    # the grouped sums from the re-encoded intermediates equal the fixed-format chain's
+    g1 = ms.to_u64_numpy(ms.agg_sum_grouped(chosen["gid"][1], chosen["m1p"][1], 1000))
+    g2 = ms.to_u64_numpy(ms.agg_sum_grouped(chosen["gid"][1], chosen["m2p"][1], 1000))
+    assert np.array_equal(g1, g["g1"]) and np.array_equal(g2, g["g2"])
+
+
 def test_c4_full():
     ms = get_ms()
     a = anchors()["c4"]

@@ -4,6 +4,8 @@ choice it drives (every candidate's size equals the oracle's footprint of the
 canonical image), intersect / merge of positions, equi-join, group ids and
 extents, elementwise arithmetic — over every input format, ragged sizes and the
 degenerate cases (empty inputs, disjoint ranges, duplicates, NotSorted)."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -14,7 +16,10 @@ from tests.gpu_util import assert_same_image, get_ms, oracle_fmt, rand_values, t
 
 pytestmark = pytest.mark.gpu
 
-IN_FMTS = ("uncompr", "static", "dyn512", "for128", "delta2048", "rle")
+
+@pytest.fixture
+def rng(request):
+    return np.random.default_rng(zlib.crc32(request.node.name.encode()))
 
 
 def fmt_of(ms, name):
