@@ -154,8 +154,8 @@ MS_API ms_status ms_decompress(const ms_ctx *ctx, const ms_column *in, uint64_t 
 /* morph: change the representation to fmt without a device round trip through
  * an uncompressed column (direct morphing): per tile decode(A) ->
  * encode(B). The result is byte-identical to compress(decompress(in), fmt)
- * (S:158); morph(x, x.fmt) is byte-identical to x. Exception noted in
- * a morph INTO MS_RLE stages through an uncompressed buffer. */
+ * (S:158); morph(x, x.fmt) is byte-identical to x. Every path decodes
+ * the input tile by tile (no uncompressed copy of the column; DP3). */
 MS_API ms_status ms_morph(const ms_ctx *ctx, const ms_column *in, ms_fmt fmt, ms_column *out);
 
 /* select: positions row_offset + i of the rows i whose value satisfies pred,

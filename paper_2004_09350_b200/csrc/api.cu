@@ -785,13 +785,47 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
     if (st != MS_OK) release(ctx, out);
     return st;
   }
-  if (fmt.format == MS_RLE) {  // staged through an uncompressed buffer
-    uint64_t* tmp = (uint64_t*)ctx.alloc(8 * (n ? n : 1));
-    if (!tmp) return MS_E_NOMEM;
-    ms_status st = ms_decompress(ctx_, in, tmp);
-    if (st == MS_OK) st = compress_rle(ctx, tmp, n, out);
-    ctx.free(tmp);
-    return st;
+  if (fmt.format == MS_RLE) {  // tile by tile from the decoded input (plan.cu), no staging column
+    const uint64_t T = (n + kChunk - 1) / kChunk;
+    Scratch sc(ctx);
+    const uint64_t o_meta = sc.add(64, true);
+    const uint64_t o_cnt = sc.add(4 * (T + 1), false);
+    const uint64_t o_fl = sc.add(16 * (T + 1), false);
+    const uint64_t o_off = sc.add(8 * (T + 2), true);
+    const uint64_t o_st = sc.add(8 * ((T + kChunk - 1) / kChunk + 1), true);
+    const uint64_t o_tk = sc.add(8, true);
+    RlePrep rp;
+    plan_rle(sc, in, rp);
+    if (!sc.commit()) return MS_E_NOMEM;
+    uint32_t* err = sc.at<uint32_t>(o_meta);
+    ColView src = view_of(in);
+    MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+    MS_TRY_CUDA(launch_rle_count_col(src, sc.at<uint32_t>(o_cnt), sc.at<uint64_t>(o_fl), ctx.s));
+    MS_TRY_CUDA(launch_count_scan(sc.at<uint32_t>(o_cnt), T, sc.at<uint64_t>(o_off), sc.at<uint64_t>(o_st),
+                                  sc.at<uint32_t>(o_tk), ctx.s));
+    uint64_t h[2] = {0, 0};
+    if (T) MS_TRY_CUDA(cudaMemcpyAsync(&h[1], sc.at<uint64_t>(o_off) + T, 8, cudaMemcpyDeviceToHost, ctx.s));
+    MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 1));
+    MS_TRY(status_from_bits((uint32_t)h[0]));
+    const uint64_t R = h[1];
+    ms_fmt f{MS_RLE, 0, 0, 0};
+    MS_TRY(alloc_column(ctx, out, f, n, 2 * R, R));
+    out->payload_words = 2 * R;
+    uint64_t* starts = (uint64_t*)ctx.alloc(8 * (R + 1));
+    if (!starts) {
+      release(ctx, out);
+      return MS_E_NOMEM;
+    }
+    cudaError_t e = launch_rle_write_col(src, sc.at<uint64_t>(o_fl), sc.at<uint64_t>(o_off), out->payload, starts,
+                                         ctx.s);
+    if (e == cudaSuccess) e = launch_rle_len(starts, R, n, out->payload, ctx.s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.s);
+    ctx.free(starts);
+    if (e != cudaSuccess) {
+      release(ctx, out);
+      return cuda_status(e);
+    }
+    return MS_OK;
   }
   const uint64_t items = (n + kChunk - 1) / kChunk;
   Scratch sc(ctx);

@@ -146,6 +146,11 @@ cudaError_t launch_join_probe(const ColView& probe, uint32_t* state, uint64_t* k
                               const uint64_t* off, const uint64_t* rows, uint32_t* tile_cnt, const uint64_t* tile_off,
                               uint64_t* out_probe, uint64_t* out_build, bool write, uint32_t* err, cudaStream_t s);
 cudaError_t launch_calc(const ColView& a, const ColView& b, int op, uint64_t* out, cudaStream_t s);
+// RLE encoding from a column source (morph into RLE): counts per 2048-row tile (first_last: 2 u64 per
+// tile), then, after the scan of the counts, (value, start) of every run
+cudaError_t launch_rle_count_col(const ColView& c, uint32_t* counts, uint64_t* first_last, cudaStream_t s);
+cudaError_t launch_rle_write_col(const ColView& c, const uint64_t* first_last, const uint64_t* tile_off,
+                                 uint64_t* payload, uint64_t* starts, cudaStream_t s);
 
 int num_sms();
 // largest block width max(cw[b+1] - cw[b]) into *out (zero-initialised)

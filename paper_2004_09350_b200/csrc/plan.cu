@@ -424,6 +424,84 @@ __global__ void __launch_bounds__(kThreads) calc_kernel(ColView a, ColView b, in
 
 inline uint64_t grid_min(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// ------------------------------------------------------------ RLE encoding of a column source
+// morph into RLE tile by tile (no uncompressed staging of the input, DP3): pass 1
+// counts the run starts inside each 2048-row tile and records the tile's first /
+// last value; rle_fix adds the starts at tile boundaries; after the scan, pass 2
+// decodes the tile again and writes (value, start) of every run at its index.
+__global__ void __launch_bounds__(kThreads) rle_count_col_kernel(ColView c, uint32_t* counts, uint64_t* first_last) {
+  __shared__ EngineSmem sm;
+  __shared__ uint32_t wsum[kThreads / 32];
+  const uint64_t T = (c.n + kChunk - 1) / kChunk;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
+    load_rows(c, r0, cnt, sm);
+    uint32_t k = 0;
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) k += i == 0 ? (t == 0) : (sm.vals[i] != sm.vals[i - 1]);
+    k = (uint32_t)warp_sum(k);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t s = 0;
+      for (int q = 0; q < kThreads / 32; ++q) s += wsum[q];
+      counts[t] = s;
+      first_last[2 * t] = sm.vals[0];
+      first_last[2 * t + 1] = sm.vals[cnt - 1];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void rle_fix_kernel(uint32_t* counts, const uint64_t* first_last, uint64_t T) {
+  for (uint64_t t = 1 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x)
+    counts[t] += first_last[2 * t] != first_last[2 * t - 1];
+}
+
+__global__ void __launch_bounds__(kThreads) rle_write_col_kernel(ColView c, const uint64_t* first_last,
+                                                                 const uint64_t* tile_off, uint64_t* payload,
+                                                                 uint64_t* starts) {
+  __shared__ EngineSmem sm;
+  __shared__ uint32_t wcnt[kThreads / 32 + 1];
+  const uint64_t T = (c.n + kChunk - 1) / kChunk;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t r0 = t * kChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kChunk, c.n - r0);
+    load_rows(c, r0, cnt, sm);
+    uint64_t base = tile_off[t];
+    // rows in order, 256 at a time: ballot per warp, warp offsets by a small scan
+    for (uint32_t i0 = 0; i0 < cnt; i0 += kThreads) {
+      const uint32_t i = i0 + threadIdx.x;
+      bool st = false;
+      if (i < cnt) {
+        const uint64_t prev = i > 0 ? sm.vals[i - 1] : (t > 0 ? first_last[2 * t - 1] : ~sm.vals[0]);
+        st = sm.vals[i] != prev;
+      }
+      const uint32_t bal = __ballot_sync(kFull, st);
+      if (lane == 0) wcnt[wid] = __popc(bal);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int q = 0; q < kThreads / 32; ++q) {
+          const uint32_t x = wcnt[q];
+          wcnt[q] = s;
+          s += x;
+        }
+        wcnt[kThreads / 32] = s;
+      }
+      __syncthreads();
+      if (st) {
+        const uint64_t idx = base + wcnt[wid] + __popc(bal & ((1u << lane) - 1u));
+        payload[2 * idx] = sm.vals[i];
+        starts[idx] = r0 + i;
+      }
+      base += wcnt[kThreads / 32];
+      __syncthreads();
+    }
+  }
+}
+
 template <class K>
 int tiles_grid(K k, uint64_t n) {
   return persistent_grid(k, kThreads, (n + kChunk - 1) / kChunk);
@@ -546,6 +624,29 @@ cudaError_t launch_join_probe(const ColView& probe, uint32_t* state, uint64_t* k
     join_probe_kernel<false><<<tiles_grid(join_probe_kernel<false>, probe.n), kThreads, 0, s>>>(
         probe, h, cnt, off, rows, tile_cnt, tile_off, out_probe, out_build, err);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rle_count_col(const ColView& c, uint32_t* counts, uint64_t* first_last, cudaStream_t s) {
+  const uint64_t T = (c.n + kChunk - 1) / kChunk;
+  if (!T) return cudaSuccess;
+  {
+    ProfScope prof_("rle_count_col", s);
+    rle_count_col_kernel<<<tiles_grid(rle_count_col_kernel, c.n), kThreads, 0, s>>>(c, counts, first_last);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || T < 2) return e;
+  ProfScope prof_("rle_fix", s);
+  rle_fix_kernel<<<(int)grid_min((T + 255) / 256, 1024), 256, 0, s>>>(counts, first_last, T);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rle_write_col(const ColView& c, const uint64_t* first_last, const uint64_t* tile_off,
+                                 uint64_t* payload, uint64_t* starts, cudaStream_t s) {
+  if (!c.n) return cudaSuccess;
+  ProfScope prof_("rle_write_col", s);
+  rle_write_col_kernel<<<tiles_grid(rle_write_col_kernel, c.n), kThreads, 0, s>>>(c, first_last, tile_off, payload,
+                                                                                  starts);
   return cudaGetLastError();
 }
 
