@@ -169,10 +169,47 @@ __device__ __forceinline__ uint32_t half_rows(const uint32_t* __restrict__ p, co
   return m;
 }
 
+// W > 32, a code-domain interval [a, a + s] inside [0, 2^32): a code matches iff
+// its low 32 bits are in the interval AND its high W - 32 bits are zero. The
+// low-word test runs for every row (one funnel shift, one add, one compare); the
+// high bits are checked only for the candidates it leaves (at most as many as the
+// matches plus the rare rows whose low word alone falls in the interval).
+template <int W, int H>
+__device__ __forceinline__ uint32_t half_low32(const uint32_t* __restrict__ p, uint32_t a, uint32_t s) {
+  constexpr int B0 = H * 16 * W;
+  constexpr int Q0 = B0 >> 5;
+  constexpr int NW = ((B0 & 31) + 16 * W + 31) / 32 + 1;
+  uint32_t r[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) r[i] = (Q0 + i < W) ? p[Q0 + i] : 0u;
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int bit = (B0 & 31) + i * W, q = bit >> 5, sh = bit & 31;
+    const uint32_t lo = sh ? __funnelshift_r(r[q], r[q + 1], sh) : r[q];
+    m |= ((lo - a) <= s ? 1u : 0u) << (i + 16 * H);
+  }
+  return m;
+}
+
 template <int W>
 __device__ __forceinline__ uint32_t lane_rows_wide(const uint32_t* __restrict__ p, const FastPred& pr,
                                                    uint64_t ref) {
   const uint64_t d = pr.lo - ref;
+  if (!pr.is_bitmap && d + pr.span >= d && d + pr.span <= 0xffffffffull) {
+    uint32_t cand = half_low32<W, 0>(p, (uint32_t)d, (uint32_t)pr.span) | half_low32<W, 1>(p, (uint32_t)d,
+                                                                                           (uint32_t)pr.span);
+    uint32_t m = cand;
+    while (cand) {  // confirm: the high W - 32 bits of the candidate's code are zero
+      const uint32_t i = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint32_t bit = i * W + 32, q = bit >> 5, sh = bit & 31;
+      uint64_t hi = (uint64_t)p[q] >> sh;
+      if (sh + (W - 32) > 32) hi |= (uint64_t)p[q + 1] << (32 - sh);
+      if (hi & ((1ull << (W - 32)) - 1)) m &= ~(1u << i);
+    }
+    return pr.neg ? ~m : m;
+  }
   return half_rows<W, 0>(p, pr, ref, d) | half_rows<W, 1>(p, pr, ref, d);
 }
 
