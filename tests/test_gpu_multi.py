@@ -51,7 +51,9 @@ def _worker(rank, world, port, q):
         wrap = torch.tensor([-(1 << 63)], dtype=torch.int64, device=dev)  # 2^63 from every rank
         D.allreduce_u64_sum(wrap)
         mx = D.max_over_ranks(float(rank + 1), dev)
-        q.put((rank, start, end, counts, pos.images(), yp.images(), ms.u64(s), ms.u64(wrap), mx))
+        gcol, ka, cw_off = D.reblock_positions(pos)  # K11: this rank's slice of the global column
+        q.put((rank, start, end, counts, pos.images(), yp.images(), ms.u64(s), ms.u64(wrap), mx,
+               (gcol.images(), cw_off)))
     finally:
         dist.destroy_process_group()
 
@@ -81,7 +83,10 @@ def _check(res, world):
     expect_pos = O.decode(opos)
     expect_sum = O.agg_sum(O.project(Y, opos, 0, O.FOR_BP, 0, 512))
     assert sum(counts) == opos.n
-    for rank, start, end, _, pimg, yimg, s, wrap, mx in res:
+    glob = _assemble([r[9] for r in res])  # K11: the re-blocked global column
+    for sec in ("payload", "cw", "ref", "rem"):
+        assert np.array_equal(glob[sec], getattr(opos, sec)), ("K11", sec)
+    for rank, start, end, _, pimg, yimg, s, wrap, mx, _g in res:
         m = end - start
         sx = O.encode(synth.gen_host("c5.X", m, start), O.DYN_BP, 0, 512)
         sy = O.encode(synth.gen_host("c5.Y", m, start), O.FOR_BP, 0, 512)
@@ -105,3 +110,46 @@ def test_nccl_world_size_1():
                     reason="needs 2 GPUs (one process per GPU)")
 def test_nccl_world_size_2():
     _check(_run(2), 2)
+
+
+def _assemble(parts):
+    """Global image from the ranks' re-blocked slices: payloads and refs in rank
+    order, cw shifted by each rank's offset, the remainder from the last rank."""
+    pay, cw, ref = [], [np.zeros(1, np.uint32)], []
+    for img, off in parts:
+        pay.append(img["payload"])
+        cw.append((img["cw"][1:].astype(np.uint64) + np.uint64(off)).astype(np.uint32))
+        ref.append(img["ref"])
+    return {"payload": np.concatenate(pay), "cw": np.concatenate(cw), "ref": np.concatenate(ref),
+            "rem": parts[-1][0]["rem"]}
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("sel", [1 << 16, 1 << 9, 3])
+def test_k11_global_reblocking_emulated(G, sel):
+    """K11: G row-range shards selected on one GPU, then re-blocked
+    into ONE global DELTA_BP{512} column (heads from the predecessors' tails, cw
+    offsets from the ranks' width totals) — byte-identical to the single-column
+    oracle image, including shards that own no full block (sel = 3: a handful of
+    matches in the whole column)."""
+    from paper_2004_09350_b200 import dist as D
+    from paper_2004_09350_b200 import ms
+    n = (1 << 21) + 2048 * 7 + 333
+    contrib = []
+    for s in range(G):
+        start, end = D.shard_range(n, G, s)
+        X = ms.compress(synth.gen_torch("c5.X", end - start, start=start), ms.dyn_bp(512))
+        pos = ms.select(X, ms.LT, sel, row_offset=start, out_fmt=ms.delta_bp(512))
+        contrib.append(D.reblock_contribution(pos))
+    counts = [c[0] for c in contrib]
+    tails = [c[1] for c in contrib]
+    parts, wsum = [], 0
+    for s in range(G):
+        col, ka = D.reblock_local(contrib[s][2], s, counts, tails)
+        parts.append((col.images(), wsum))
+        wsum += col.payload_words * 64 // 512
+    got = _assemble(parts)
+    X = O.encode(synth.gen_host("c5.X", n), O.DYN_BP, 0, 512)
+    want = O.select(X, O.LT, sel, out_fmt=O.DELTA_BP, out_block=512)
+    for sec in ("payload", "cw", "ref", "rem"):
+        assert np.array_equal(got[sec], getattr(want, sec)), (G, sel, sec)
