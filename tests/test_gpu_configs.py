@@ -354,3 +354,48 @@ def test_c5_eight_shards_full():
     offs = D.exclusive_offsets(counts)
     assert offs[0] == 0 and offs[1] == a["shard_counts_g8"][0] and offs[-1] + counts[-1] == a["count"]
     assert total % (1 << 64) == a["sum_projected"]
+
+
+# ------------------------------------------------------------------ sharded c2 / c4
+@pytest.mark.parametrize("G", [3])
+def test_c2_sharded_full(G):
+    """BJ.c2 cut into G row-range shards (D-18), one after another on one GPU:
+    the C1 counts and the C2 sums combine to the full-size anchors."""
+    ms = get_ms()
+    from paper_2004_09350_b200 import dist as D
+    a = anchors()["c2"]
+    n = a["n"]
+    count, total = 0, 0
+    for s in range(G):
+        start, end = D.shard_range(n, G, s)
+        X, Y, pos, yp, yu = c2_chain(ms, end - start, start)
+        count += pos.n
+        total += ms.u64(ms.agg_sum(yp))
+        assert ms.u64(ms.agg_sum(yp)) == ms.u64(ms.agg_sum(yu))
+        del X, Y, pos, yp, yu
+    assert count == a["count"]
+    assert total % (1 << 64) == a["sum_projected"]
+
+
+@pytest.mark.parametrize("G", [4])
+def test_c4_sharded_full(G):
+    """BJ.c4's D-16 chain on G row-range shards: the per-shard 1000-group sums
+    added element-wise (the C3 allreduce of SURVEY.md §8(e)) equal the anchors."""
+    ms = get_ms()
+    from paper_2004_09350_b200 import dist as D
+    a = anchors()["c4"]
+    n = a["n"]
+    g1 = np.zeros(1000, np.uint64)
+    g2 = np.zeros(1000, np.uint64)
+    c1 = c2 = 0
+    for s in range(G):
+        start, end = D.shard_range(n, G, s)
+        g = c4_chain(ms, end - start, start)
+        g1 += g["g1"]
+        g2 += g["g2"]
+        c1 += g["pos1"].n
+        c2 += g["pos2"].n
+        del g
+    assert c1 == a["count_pos1"] and c2 == a["count_pos2"]
+    assert [int(x) for x in g1] == a["grouped_m1"]
+    assert [int(x) for x in g2] == a["grouped_m2"]
