@@ -246,6 +246,17 @@ MS_API ms_status ms_group(const ms_ctx *ctx, const ms_column *keys, const ms_col
 MS_API ms_status ms_join(const ms_ctx *ctx, const ms_column *left, const ms_column *right, ms_fmt left_fmt,
                          ms_fmt right_fmt, ms_column *out_left, ms_column *out_right);
 
+/* Semi-join against a key bitmap (BJ.c4's star-schema join, D-16):
+ * out = the positions p of `positions` (sorted row ids, global: row_offset + row
+ * of `keys`) whose key keys[p - row_offset] is in the bitmap (bit k of bitmap[k/64]
+ * for k < bitmap_bits), in out_fmt. Equal to project(positions, select(project(
+ * keys, positions), IN_BITMAP)) — the fused form (K7) gathers the keys of each
+ * 512-position block into shared memory and tests them there, so the projected
+ * keys are never written. MS_E_RANGE if a position lies outside the keys. */
+MS_API ms_status ms_semijoin(const ms_ctx *ctx, const ms_column *keys, const ms_column *positions,
+                             uint64_t row_offset, const uint64_t *bitmap, uint64_t bitmap_bits, ms_fmt out_fmt,
+                             ms_column *out);
+
 /* Elementwise arithmetic mod 2^64 (star-schema measures such as
  * price x discount): out[i] = a[i] op b[i], op = MS_ADD / MS_SUB / MS_MUL.
  * MS_E_INVALID if a->n != b->n (LengthMismatch) or op is unknown. */

@@ -1367,6 +1367,49 @@ ms_status ms_calc(const ms_ctx* ctx_, int32_t op, const ms_column* a, const ms_c
   return ms_compress(ctx_, sc.at<uint64_t>(o_out), n, out_fmt, out);
 }
 
+ms_status ms_semijoin(const ms_ctx* ctx_, const ms_column* keys, const ms_column* positions, uint64_t row_offset,
+                      const uint64_t* bitmap, uint64_t bitmap_bits, ms_fmt out_fmt, ms_column* out) {
+  if (!out) return MS_E_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  MS_TRY(check_col(keys));
+  MS_TRY(check_col(positions));
+  MS_TRY(check_fmt(out_fmt));
+  if (bitmap_bits && !bitmap) return MS_E_INVALID;
+  const int32_t pf = positions->fmt.format, kf = keys->fmt.format;
+  const bool fused = (pf == MS_UNCOMPR || pf == MS_STATIC_BP || pf == MS_DYN_BP || pf == MS_FOR_BP ||
+                      (pf == MS_DELTA_BP && positions->fmt.block_size == (uint32_t)kSegRows)) &&
+                     (kf == MS_UNCOMPR || kf == MS_STATIC_BP || kf == MS_DYN_BP || kf == MS_FOR_BP);
+  Ctx ctx(ctx_);
+  const uint64_t n1 = positions->n;
+  if (!fused) {  // the operator-at-a-time chain (D-16): project, select IN_BITMAP, project
+    ms_column kp, idx;
+    MS_TRY(ms_project(ctx_, keys, positions, row_offset, ms_fmt{MS_UNCOMPR, 0, 0, 0}, &kp));
+    ms_pred p{MS_IN_BITMAP, 0, 0, 0, bitmap, bitmap_bits};
+    ms_status st = ms_select(ctx_, &kp, &p, 0, ms_fmt{MS_DELTA_BP, 0, 512, 0}, &idx);
+    release(ctx, &kp);
+    if (st != MS_OK) return st;
+    st = ms_project(ctx_, positions, &idx, 0, out_fmt, out);
+    release(ctx, &idx);
+    return st;
+  }
+  const uint64_t NS = (n1 + kSegRows - 1) / kSegRows;
+  Scratch sc(ctx);
+  const uint64_t o_meta = sc.add(64, true);
+  const uint64_t o_bits = sc.add(4 * NS * kSegWords, false);
+  const uint64_t o_seg = sc.add(4 * (NS + 1), false);
+  if (!sc.commit()) return MS_E_NOMEM;
+  uint32_t* err = sc.at<uint32_t>(o_meta);
+  MS_TRY_CUDA(launch_semi_mask(view_of(positions), view_of(keys), row_offset, bitmap, bitmap_bits,
+                               sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), err, ctx.s));
+  // the surviving ranks of pos1 (DELTA_BP{512}, the select output layer), then pos1 at those ranks
+  ms_column idx;
+  MS_TRY(positions_from_mask(ctx, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, n1, 0,
+                             ms_fmt{MS_DELTA_BP, 0, 512, 0}, err, &idx));
+  const ms_status st = ms_project(ctx_, positions, &idx, 0, out_fmt, out);
+  release(ctx, &idx);
+  return st;
+}
+
 ms_status ms_check_errors(const ms_ctx* ctx_) {
   Ctx ctx(ctx_);
   uint32_t h = 0;

@@ -108,6 +108,7 @@ def _load():
         "ms_group": ([P(_Ctx), C, C, u64, _Fmt, _Fmt, C, C], st),
         "ms_join": ([P(_Ctx), C, C, _Fmt, _Fmt, C, C], st),
         "ms_calc": ([P(_Ctx), ctypes.c_int32, C, C, _Fmt, C], st),
+        "ms_semijoin": ([P(_Ctx), C, C, u64, vp, u64, _Fmt, C], st),
         "ms_column_release": ([P(_Ctx), C], None),
         "ms_column_bytes": ([C], u64),
         "ms_status_str": ([ctypes.c_int], ctypes.c_char_p),
@@ -441,6 +442,17 @@ def join(left: Column, right: Column, left_fmt=None, right_fmt=None, stream=None
                         _fmt(left_fmt or uncompr()), _fmt(right_fmt or uncompr()), ctypes.byref(lo),
                         ctypes.byref(ro)), "ms_join")
     return Column(lo, stream=s), Column(ro, stream=s)
+
+
+def semijoin(keys: Column, positions: Column, bitmap: torch.Tensor, bitmap_bits: int, row_offset: int = 0,
+             out_fmt=None, stream=None) -> Column:
+    """ms_semijoin: the positions whose key is in the bitmap (fused K7 when the formats allow)."""
+    out = _Column()
+    s = _uses(stream, keys, positions)
+    _check(_lib.ms_semijoin(ctypes.byref(_ctx(stream)), ctypes.byref(keys._c), ctypes.byref(positions._c),
+                            row_offset, _ptr(bitmap), bitmap_bits, _fmt(out_fmt or delta_bp(512)),
+                            ctypes.byref(out)), "ms_semijoin")
+    return Column(out, stream=s)
 
 
 def calc(op: int, a: Column, b: Column, out_fmt=None, stream=None) -> Column:

@@ -15,7 +15,7 @@ import pytest
 
 import oracle as O
 import synth
-from tests.gpu_util import assert_same_image, get_ms, to_torch
+from tests.gpu_util import assert_same_image, get_ms, oracle_fmt, to_torch
 
 pytestmark = pytest.mark.gpu
 
@@ -399,3 +399,43 @@ def test_c4_sharded_full(G):
     assert c1 == a["count_pos1"] and c2 == a["count_pos2"]
     assert [int(x) for x in g1] == a["grouped_m1"]
     assert [int(x) for x in g2] == a["grouped_m2"]
+
+
+# ------------------------------------------------------------------ K7: fused semi-join (D-16)
+def test_c4_semijoin_fused_reduced():
+    """ms_semijoin (gather k1 at pos1 in shared memory, bitmap test, surviving
+    ranks, pos1 at those ranks) is byte-identical to the oracle's operator-at-a-time
+    D-16 chain pos2 = project(pos1, select(project(k1, pos1), IN_BITMAP)); the
+    non-fused fallback (keys without O(1) access) gives the same bytes."""
+    ms = get_ms()
+    n = 1 << 22
+    D4 = synth.D4
+    bm_host = synth.bitmap_c4()
+    bm = to_torch(bm_host)
+    k0 = ms.compress(dev("c4.k0", n), ms.static_bp(12))
+    k1 = ms.compress(dev("c4.k1", n), ms.static_bp(18))
+    pos1 = ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512))
+    ok0 = O.encode(synth.gen_host("c4.k0", n), O.STATIC_BP, 12)
+    ok1 = O.encode(synth.gen_host("c4.k1", n), O.STATIC_BP, 18)
+    opos1 = O.select(ok0, O.BETWEEN, 0, 365, out_fmt=O.DELTA_BP, out_block=512)
+    oidx = O.select(O.project(ok1, opos1, 0, O.STATIC_BP, 18, 0), O.IN_BITMAP, bitmap=bm_host, bitmap_bits=D4[1],
+                    out_fmt=O.DELTA_BP, out_block=512)
+    for fo in (ms.delta_bp(512), ms.uncompr()):
+        opos2 = O.project(opos1, oidx, 0, *oracle_fmt(fo))
+        assert_same_image(ms.semijoin(k1, pos1, bm, D4[1], out_fmt=fo), opos2, f"K7 fused -> {fo}")
+    k1d = ms.morph(k1, ms.delta_bp(2048))  # no O(1) row access: the operator chain
+    opos2 = O.project(opos1, oidx, 0, O.DELTA_BP, 0, 512)
+    assert_same_image(ms.semijoin(k1d, pos1, bm, D4[1]), opos2, "K7 fallback chain")
+
+
+def test_c4_semijoin_fused_full():
+    ms = get_ms()
+    a = anchors()["c4"]
+    n = a["n"]
+    bm = to_torch(synth.bitmap_c4())
+    k0 = ms.compress(dev("c4.k0", n), ms.static_bp(12))
+    k1 = ms.compress(dev("c4.k1", n), ms.static_bp(18))
+    pos1 = ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512))
+    pos2 = ms.semijoin(k1, pos1, bm, synth.D4[1])
+    assert pos2.n == a["count_pos2"]
+    assert pos2.footprint() == a["pos2_bytes"]
