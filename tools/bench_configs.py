@@ -137,8 +137,20 @@ def c4(reps):
         gid = ms.project(gattr, k3p, 0, ms.static_bp(10))
         return ms.agg_sum_grouped(gid, m1p, 1000), ms.agg_sum_grouped(gid, m2p, 1000)
 
+    def chain_fused():  # the measured path of D-16: the semi-join fused (K7)
+        pos1 = ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512))
+        pos2 = ms.semijoin(k1, pos1, bm, Dm[1])
+        m1p = ms.project(m1, pos2, 0, ms.dyn_bp(512))
+        m2p = ms.project(m2, pos2, 0, ms.dyn_bp(512))
+        k3p = ms.project(k3, pos2, 0, ms.static_bp(17))
+        gid = ms.project(gattr, k3p, 0, ms.static_bp(10))
+        return ms.agg_sum_grouped(gid, m1p, 1000), ms.agg_sum_grouped(gid, m2p, 1000)
+
     alg = k0.footprint() + k1.footprint() + m1.footprint() + m2.footprint() + k3.footprint()
-    report("c4", "full chain (select, semi-join, projects, grouped sums)", timed(chain, reps), n, alg)
+    report("c4", "full chain, fused semi-join K7 (select, semi-join, projects, grouped sums)",
+           timed(chain_fused, reps), n, alg)
+    report("c4", "full chain, operator at a time (select, project, select, project, ...)", timed(chain, reps), n,
+           alg)
     pos1 = ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512))
     report("c4", "select k0 in [0,365) -> DELTA_BP{512}",
            timed(lambda: ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512)), reps), n,
