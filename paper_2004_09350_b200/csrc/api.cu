@@ -701,6 +701,12 @@ ms_status ms_decompress(const ms_ctx* ctx_, const ms_column* in, uint64_t* value
   uint32_t* err = sc.at<uint32_t>(o_meta);
   ColView src = view_of(in);
   MS_TRY_CUDA(run_rle(sc, in, rp, src, err));
+  if (delta_direct_supported(src)) {  // lanes of 64 rows, no CTA-wide scan (delta.cu)
+    MS_TRY_CUDA(launch_delta_decode(src, values, err, ctx.s));
+    uint64_t h = 0;
+    MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), &h, 1));
+    return status_from_bits((uint32_t)h);
+  }
   if (in->fmt.format == MS_RLE) {  // runs expanded directly, no tile decode
     MS_TRY_CUDA(launch_rle_expand(in->payload, src.run_starts, in->n_runs, in->n, values, ctx.s));
     uint64_t h = 0;
@@ -736,6 +742,33 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
       return cuda_status(e);
     }
     return MS_OK;
+  }
+  if (delta_direct_supported(view_of(in)) && (fmt.format == MS_STATIC_BP || fmt.format == MS_UNCOMPR)) {
+    // DELTA_BP -> STATIC_BP / UNCOMPR directly (delta.cu): [max pass for the auto width,]
+    // then every output word written once
+    Scratch sc(ctx);
+    const uint64_t o_meta = sc.add(64, true);  // [0] err, [1] max
+    if (!sc.commit()) return MS_E_NOMEM;
+    uint32_t* err = sc.at<uint32_t>(o_meta);
+    const ColView v = view_of(in);
+    ms_fmt f = fmt;
+    if (f.format == MS_STATIC_BP && f.bit_width == 0) {
+      MS_TRY_CUDA(launch_delta_max(v, sc.at<unsigned long long>(o_meta + 8), err, ctx.s));
+      uint64_t h[2];
+      MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
+      MS_TRY(status_from_bits((uint32_t)h[0]));
+      f.bit_width = ebw_host(h[1]) ? ebw_host(h[1]) : 1;
+    }
+    const uint64_t words = f.format == MS_UNCOMPR ? n : words_for(n, f.bit_width);
+    MS_TRY(alloc_column(ctx, out, f, n, words, 0));
+    out->payload_words = words;
+    cudaError_t e = f.format == MS_UNCOMPR ? launch_delta_decode(v, out->payload, err, ctx.s)
+                                           : launch_delta_to_static(v, f.bit_width, out->payload, err, ctx.s);
+    uint64_t h = 0;
+    ms_status st = e == cudaSuccess ? readback(ctx, sc.at<uint64_t>(o_meta), &h, 1) : cuda_status(e);
+    if (st == MS_OK) st = status_from_bits((uint32_t)h);
+    if (st != MS_OK) release(ctx, out);
+    return st;
   }
   if (in->fmt.format == MS_RLE && fmt.format == MS_DELTA_BP) {
     // direct morph: from the runs alone (morph.cu)

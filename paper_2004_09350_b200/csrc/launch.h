@@ -156,6 +156,13 @@ cudaError_t launch_rle_count_col(const ColView& c, uint32_t* counts, uint64_t* f
 cudaError_t launch_rle_write_col(const ColView& c, const uint64_t* first_last, const uint64_t* tile_off,
                                  uint64_t* payload, uint64_t* starts, cudaStream_t s);
 
+// DELTA_BP (B >= 128) decoded by lanes of 64 rows (delta.cu): into u64 values, its maximum, or a
+// static-BP stream at width ws (every payload word written; MS_E_WIDTH_OVERFLOW if a value needs more)
+bool delta_direct_supported(const ColView& c);
+cudaError_t launch_delta_decode(const ColView& c, uint64_t* out, uint32_t* err, cudaStream_t s);
+cudaError_t launch_delta_max(const ColView& c, unsigned long long* max_out, uint32_t* err, cudaStream_t s);
+cudaError_t launch_delta_to_static(const ColView& c, uint32_t ws, uint64_t* payload, uint32_t* err, cudaStream_t s);
+
 int num_sms();
 // largest block width max(cw[b+1] - cw[b]) into *out (zero-initialised)
 cudaError_t launch_max_width(const uint32_t* cw, uint64_t nb, uint32_t* out, cudaStream_t s);
