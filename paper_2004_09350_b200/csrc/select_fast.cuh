@@ -119,11 +119,27 @@ __device__ __forceinline__ uint32_t lane_rows(const uint32_t* __restrict__ p, co
     } else if constexpr (W <= 32) {
       uint32_t a, sp, ng;
       code_interval(pr.lo, pr.span, pr.neg, ref, W, a, sp, ng);
+      constexpr uint32_t cmask = W >= 32 ? 0xffffffffu : ((1u << (W & 31)) - 1u);
+      if (a == 0 && (sp & (sp + 1)) == 0 && sp < cmask) {
+        // prefix interval [0, 2^k): a code matches iff its bits k..W-1 are zero — one
+        // AND with a shifted mask per row, no extraction of the code (the specialized-
+        // operator shortcut of P:352 applied to the bit layout)
+        const uint32_t hi = cmask & ~sp;  // the code's high bits
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t c = (uint32_t)code_at<W>(r, i);
-        const bool keep = ((c - a) <= sp) != (ng != 0);
-        m |= (keep ? 1u : 0u) << i;
+        for (int i = 0; i < 32; ++i) {
+          const int bit = i * W, q = bit >> 5, sh = bit & 31;
+          bool z;
+          if (sh + W <= 32) z = (r[q] & (hi << sh)) == 0u;
+          else z = (__funnelshift_r(r[q], r[q + 1], sh) & hi) == 0u;
+          m |= (z != (ng != 0) ? 1u : 0u) << i;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t c = (uint32_t)code_at<W>(r, i);
+          const bool keep = ((c - a) <= sp) != (ng != 0);
+          m |= (keep ? 1u : 0u) << i;
+        }
       }
     } else {
       const uint64_t d = pr.lo - ref;
