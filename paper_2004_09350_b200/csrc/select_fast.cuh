@@ -131,16 +131,16 @@ __device__ __forceinline__ uint32_t lane_rows(const uint32_t* __restrict__ p, co
           bool z;
           if (sh + W <= 32) z = (r[q] & (hi << sh)) == 0u;
           else z = (__funnelshift_r(r[q], r[q + 1], sh) & hi) == 0u;
-          m |= (z != (ng != 0) ? 1u : 0u) << i;
+          if (z) m |= 1u << i;  // (a predicated OR with a constant)
         }
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const uint32_t c = (uint32_t)code_at<W>(r, i);
-          const bool keep = ((c - a) <= sp) != (ng != 0);
-          m |= (keep ? 1u : 0u) << i;
+          if ((c - a) <= sp) m |= 1u << i;
         }
       }
+      if (ng) m = ~m;  // the negated predicates, once per 32 rows
     } else {
       const uint64_t d = pr.lo - ref;
 #pragma unroll
