@@ -343,6 +343,7 @@ def run_ours(args):
            "project_pipe": gather_bytes + bytes_yp,
            "project_win": gather_bytes + bytes_yp,
            "project_slot": gather_bytes + bytes_yp,                # positions + touched Y + Y' into slots
+           "project_stream": gather_bytes + bytes_yp,              # positions + touched Y + Y' into slots
            "project_copy": 2 * bytes_yp,                           # slots read, Y' written
            "project_warp": gather_bytes + bytes_yp,
            "sum_fast": bytes_yp}                                   # Y' read

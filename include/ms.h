@@ -126,6 +126,8 @@ typedef void (*ms_free_fn)(void *alloc_ctx, void *ptr, void *stream);
 #define MS_FLAG_SHRINK 1u /* copy variable-size outputs into an exact-size allocation (default: a producer
                            that sizes its output before the kernel keeps the slack of its provable capacity
                            in alloc_bytes; nothing is copied) */
+#define MS_FLAG_GATHER 2u /* ms_project: always gather the data rows sector by sector, never stream the data
+                           windows through shared memory (a measurement switch; the output is identical) */
 
 typedef struct {
   void *stream;           /* cudaStream_t */

@@ -18,6 +18,7 @@ __device__ uint32_t g_ms_sticky_err;  // errors of the non-synchronising ops
 namespace {
 
 constexpr uint64_t kAlign = 256;
+constexpr uint64_t kStreamAvgWindow = 22 * 1024;  // project: stream when the mean window (bytes) is below
 inline uint64_t align_up(uint64_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 inline bool is_block(int32_t f) { return f == MS_DYN_BP || f == MS_FOR_BP || f == MS_DELTA_BP; }
 inline bool valid_B(uint32_t B) { return B == 128 || B == 256 || B == 512 || B == 1024 || B == 2048; }
@@ -984,12 +985,23 @@ ms_status ms_project(const ms_ctx* ctx_, const ms_column* data, const ms_column*
       slots = (uint64_t*)ctx.alloc(8 * (n / G) * (uint64_t)slot_words);
       if (!slots) e = cudaErrorMemoryAllocation;
     }
+    // dense positions stream the data windows through shared memory (projstream.cuh): when the
+    // average window of an output block (the data payload over the blocks, if the positions span
+    // the column) fits a stage with room for its spread
+    void* wins = nullptr;
+    const uint64_t n_items_out = (n + G - 1) / G;
+    if (e == cudaSuccess && slots && !(ctx.c && (ctx.c->flags & MS_FLAG_GATHER)) &&
+        project_stream_supported(pv, dv, pe) && 8 * data->payload_words <= (n / G) * (uint64_t)kStreamAvgWindow) {
+      wins = ctx.alloc(project_stream_win_bytes(n_items_out));
+      if (!wins) e = cudaErrorMemoryAllocation;
+    }
     if (e == cudaSuccess)
       e = slotted ? launch_project_slots(pv, dv, row_offset, pe, slots, slot_words, sc.at<uint32_t>(o_wk),
-                                         sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3), sc.at<uint32_t>(o_tk3), err,
-                                         ctx.s)
+                                         sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3), sc.at<uint32_t>(o_tk3), wins,
+                                         8 * data->payload_words, err, ctx.s)
                   : launch_project_warp(pv, dv, row_offset, pe, sc.at<uint64_t>(o_st), sc.at<uint32_t>(o_tk), err,
                                         ctx.s);
+    ctx.free(wins);
     ctx.free(slots);
     if (e != cudaSuccess) {
       release(ctx, out);

@@ -4,6 +4,7 @@
 #include "grid.cuh"
 #include "positions.cuh"
 #include "posdelta.cuh"
+#include "projstream.cuh"
 #include "launch.h"
 
 namespace ms {
@@ -206,7 +207,8 @@ cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64
 // widths, copy the blocks to their places (pos_copy_kernel is format-agnostic).
 cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e0,
                                  uint64_t* slots, uint32_t slot_words, uint32_t* wk, uint64_t* cwx,
-                                 uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err, cudaStream_t s) {
+                                 uint64_t* scan_status, uint32_t* scan_ticket, void* stream_wins,
+                                 uint64_t data_pay_bytes, uint32_t* err, cudaStream_t s) {
   const PosEnc& e = e0;
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   const uint64_t n_full = e.n_out / e.G;
@@ -227,9 +229,28 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
     return cudaGetLastError();
   };
   const ProjectSource<4> src{pos, data, row_offset, pf};
-  cudaError_t r = e.G == 512   ? launch(warp_encode_slot_kernel<ProjectSource<4>, 16>, src)
+  cudaError_t r;
+  if (stream_wins && e.G == 512) {
+    PsWin* wins = static_cast<PsWin*>(stream_wins);
+    {
+      ProfScope prof_("project_window", s);
+      project_window_kernel<<<(int)((n_items + 255) / 256), 256, 0, s>>>(pos, data, row_offset, e.n_out,
+                                                                         data_pay_bytes, wins);
+      r = cudaGetLastError();
+    }
+    if (r != cudaSuccess) return r;
+    auto k = project_stream_kernel<kPsStages, kPsPairs>;
+    const size_t smem = ps_smem_bytes();
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t grid = n_items < (uint64_t)num_sms() ? n_items : (uint64_t)num_sms();
+    ProfScope prof_("project_stream", s);
+    k<<<(int)grid, kPsThreads, smem, s>>>(src, e, n_items, wins, slots, slot_words, wk, err);
+    r = cudaGetLastError();
+  } else {
+    r = e.G == 512   ? launch(warp_encode_slot_kernel<ProjectSource<4>, 16>, src)
                   : e.G == 256 ? launch(warp_encode_slot_kernel<ProjectSource<4>, 8>, src)
                                : launch(warp_encode_slot_kernel<ProjectSource<4>, 4>, src);
+  }
   if (r != cudaSuccess) return r;
   const bool block = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
   if (!block || !n_full) return cudaSuccess;
@@ -240,5 +261,17 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
   pos_copy_kernel<32><<<(int)cgrid, 256, 0, s>>>(e, n_full, slots, slot_words, cwx, err);
   return cudaGetLastError();
 }
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+bool project_stream_supported(const ColView& pos, const ColView& data, const PosEnc& e) {
+  const bool block_out = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
+  return block_out && e.G == 512 && e.n_out >= 512 && pos.format == MS_DELTA_BP && pos.B == 512 &&
+         (data.format == MS_DYN_BP || data.format == MS_FOR_BP) && data.B >= 64 && data.nb > 0 &&
+         aligned16(pos.payload) && aligned16(data.payload) && aligned16(data.cw) &&
+         (data.format != MS_FOR_BP || aligned16(data.ref));
+}
+
+size_t project_stream_win_bytes(uint64_t n_items) { return sizeof(PsWin) * n_items; }
 
 }  // namespace ms

@@ -88,9 +88,15 @@ cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_
 
 // project into per-block slots (G <= 512, block formats or UNCOMPR), scan of the widths, copy.
 // Scratch: slots (n/G * slot_words u64), wk (n/G u32), cwx (n/G + 1 u64), scan status (zeroed), ticket (zeroed).
+// stream_wins (64 B per item, or nullptr): the streamed variant (projstream.cuh) for dense DELTA_BP{512}
+// positions over DYN_BP / FOR_BP data; data_pay_bytes bounds its payload reads.
 cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64_t row_offset, const PosEnc& e,
                                  uint64_t* slots, uint32_t slot_words, uint32_t* wk, uint64_t* cwx,
-                                 uint64_t* scan_status, uint32_t* scan_ticket, uint32_t* err, cudaStream_t s);
+                                 uint64_t* scan_status, uint32_t* scan_ticket, void* stream_wins,
+                                 uint64_t data_pay_bytes, uint32_t* err, cudaStream_t s);
+// whether the streamed project applies (host-side shape checks; the caller adds the density rule)
+bool project_stream_supported(const ColView& pos, const ColView& data, const PosEnc& e);
+size_t project_stream_win_bytes(uint64_t n_items);
 
 // direct morph RLE -> DELTA_BP{B} (morph.cu): per-run widths / bases / remainder, then (after the
 // width scan and the exact allocation) the steps ORed into the zeroed payload and cw

@@ -478,6 +478,64 @@ __global__ void __launch_bounds__(128) warp_encode_deferred_kernel(Src src, PosE
 // reference to ref[k]; the scan of wk gives cw, and pos_copy_kernel moves each
 // block to word cw[k] * G / 64. Non-block formats and the final partial block
 // are written directly.
+// One full block of G = 32*PER values in the tile P (project's gathered values or
+// select's positions) re-encoded at its own width into its fixed-size slot
+// (slot_words u64): lane j takes ranks [PER*j, PER*j + PER) into registers,
+// forms the codes (DELTA: differences, FOR: minus the block minimum, DYN: the
+// values), packs them in place (pack_lane_codes) and stores the block; the width
+// goes to wk[item], the reference to ref[item].
+template <int PER>
+__device__ __forceinline__ void slot_encode_block(const PosEnc& e, uint64_t item, uint64_t* P,
+                                                  uint64_t* __restrict__ slots, uint32_t slot_words,
+                                                  uint32_t* __restrict__ wk, uint32_t* err, uint32_t lane) {
+  constexpr uint32_t G = 32 * PER;
+  uint64_t c[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) c[q] = P[pidx(lane * PER + q)];
+  uint64_t ref = 0, mx = 0;
+  if (e.format == MS_DELTA_BP) {
+    const uint64_t last = __shfl_up_sync(kFull, c[PER - 1], 1);
+    ref = __shfl_sync(kFull, c[0], 0);
+#pragma unroll
+    for (int q = PER - 1; q > 0; --q) c[q] -= c[q - 1];
+    c[0] = lane ? c[0] - last : 0ull;
+  } else if (e.format == MS_FOR_BP) {
+    uint64_t lo = c[0];
+#pragma unroll
+    for (int q = 1; q < PER; ++q) lo = c[q] < lo ? c[q] : lo;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t t = __shfl_xor_sync(kFull, lo, o);
+      lo = t < lo ? t : lo;
+    }
+    ref = lo;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) c[q] -= lo;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) mx = c[q] > mx ? c[q] : mx;
+  const uint32_t w = ebw64(warp_max(mx));
+  __syncwarp();
+  pack_lane_codes<PER>(reinterpret_cast<uint32_t*>(P), c, w, lane);
+  const uint32_t nw64 = G / 64 * w;
+  if (nw64 > slot_words) {  // a width above the host's bound (an understated hint)
+    if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+  } else {
+    uint64_t* dst = slots + item * slot_words;
+    for (uint32_t m = lane; m < nw64; m += 32) dst[m] = P[m];
+  }
+  if (lane == 0) {
+    wk[item] = w;
+    if (e.format != MS_DYN_BP) e.ref[item] = ref;
+  }
+  __syncwarp();
+}
+
+// Slot variant of the output-side buffer layer (no look-back at all): one tile
+// per warp, items in grid-stride order; a full block is packed at its own width
+// and written to its fixed-size slot (slot_encode_block); the scan of wk gives
+// cw, and pos_copy_kernel moves each block to word cw[k] * G / 64. Non-block
+// formats and the final partial block are written directly.
 template <class Src, int PER>
 __global__ void __launch_bounds__(128) warp_encode_slot_kernel(Src src, PosEnc e, uint64_t n_items,
                                                                uint64_t* __restrict__ slots, uint32_t slot_words,
@@ -497,46 +555,7 @@ __global__ void __launch_bounds__(128) warp_encode_slot_kernel(Src src, PosEnc e
       __syncwarp();
       continue;
     }
-    uint64_t c[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) c[q] = P[pidx(lane * PER + q)];
-    uint64_t ref = 0, mx = 0;
-    if (e.format == MS_DELTA_BP) {
-      const uint64_t last = __shfl_up_sync(kFull, c[PER - 1], 1);
-      ref = __shfl_sync(kFull, c[0], 0);
-#pragma unroll
-      for (int q = PER - 1; q > 0; --q) c[q] -= c[q - 1];
-      c[0] = lane ? c[0] - last : 0ull;
-    } else if (e.format == MS_FOR_BP) {
-      uint64_t lo = c[0];
-#pragma unroll
-      for (int q = 1; q < PER; ++q) lo = c[q] < lo ? c[q] : lo;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t t = __shfl_xor_sync(kFull, lo, o);
-        lo = t < lo ? t : lo;
-      }
-      ref = lo;
-#pragma unroll
-      for (int q = 0; q < PER; ++q) c[q] -= lo;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) mx = c[q] > mx ? c[q] : mx;
-    const uint32_t w = ebw64(warp_max(mx));
-    __syncwarp();
-    pack_lane_codes<PER>(reinterpret_cast<uint32_t*>(P), c, w, lane);
-    const uint32_t nw64 = G / 64 * w;
-    if (nw64 > slot_words) {  // a width above the host's bound (an understated hint)
-      if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
-    } else {
-      uint64_t* dst = slots + item * slot_words;
-      for (uint32_t m = lane; m < nw64; m += 32) dst[m] = P[m];
-    }
-    if (lane == 0) {
-      wk[item] = w;
-      if (e.format != MS_DYN_BP) e.ref[item] = ref;
-    }
-    __syncwarp();
+    slot_encode_block<PER>(e, item, P, slots, slot_words, wk, err, lane);
   }
 }
 

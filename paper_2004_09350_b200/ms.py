@@ -27,6 +27,7 @@ OP_NAMES = ("EQ", "NE", "LT", "LE", "GT", "GE", "BETWEEN", "IN_BITMAP")
 STATUS = ("MS_OK", "MS_E_INVALID", "MS_E_WIDTH_OVERFLOW", "MS_E_UNSUPPORTED", "MS_E_RANGE", "MS_E_CORRUPT",
           "MS_E_NOMEM", "MS_E_CUDA")
 FLAG_SHRINK = 1
+FLAG_GATHER = 2  # ms_project: never stream the data windows (measurement switch)
 
 
 class MsError(RuntimeError):
