@@ -334,6 +334,7 @@ def run_ours(args):
     # algorithmic bytes per launch: what the method itself must move
     mask_bytes = 4 * 16 * ((m + 511) // 512)                       # select's 1-bit-per-row match mask
     alg = {"select_fast": x_bytes + mask_bytes,                    # compressed X read, mask written
+           "select_stream": x_bytes + mask_bytes,
            "pos_width": mask_bytes,                                # mask read
            "pos_pack": mask_bytes + bytes_pos,                     # mask read, positions image written
            "pos_encode": mask_bytes + bytes_pos,
@@ -346,7 +347,8 @@ def run_ours(args):
            "project_stream": gather_bytes + bytes_yp,              # positions + touched Y + Y' into slots
            "project_copy": 2 * bytes_yp,                           # slots read, Y' written
            "project_warp": gather_bytes + bytes_yp,
-           "sum_fast": bytes_yp}                                   # Y' read
+           "sum_fast": bytes_yp,                                   # Y' read
+           "sum_stream": bytes_yp}
     kernels = {}
     for k, (k_launches, tot_ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         avg = tot_ms / max(1, k_launches)

@@ -78,8 +78,8 @@ typedef enum {
  * max_width: block formats: the largest block width of the column if known
  *   (1..64), 0 = unknown. Not part of the image; a sizing hint that libms
  *   producers fill in and scans use to pick narrower staging buffers. An
- *   understated hint never causes an out-of-bounds access: blocks that do not
- *   fit the chosen staging slot are reported as MS_E_CORRUPT. Ignored on
+ *   understated hint costs speed, never correctness: a chunk that does not fit
+ *   the staging buffer it sized is read from global memory instead. Ignored on
  *   output specs. */
 typedef struct {
   int32_t format;

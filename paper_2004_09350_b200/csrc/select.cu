@@ -4,6 +4,7 @@
 #include "engine.cuh"
 #include "grid.cuh"
 #include "select_fast.cuh"
+#include "selstream.cuh"
 #include "launch.h"
 
 namespace ms {
@@ -279,9 +280,22 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
     // (BJ.c5): 3-stage and 8-warp variants of the narrow kernel were 8-50% slower.
     const bool narrow = kind == FAST_UNCOMPR || (c.maxw >= 1 && c.maxw <= 32);
     const bool medium = !narrow && c.maxw >= 33 && c.maxw <= 48;
+    // narrow bit-packed columns: the CTA-streamed core (selstream.cuh)
+    const uint32_t mw = kind == FAST_STATIC ? c.w : c.maxw;
+    const bool stream = kind != FAST_UNCOMPR && mw >= 1 && mw <= 32;
+    auto pick_stream = [&](auto k) {
+      const int S = ss_stages(mw);
+      const size_t smem = ss_smem_bytes(mw, S);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const uint64_t nchunks = (ns_fast + kSsSegs - 1) / kSsSegs;
+      const int grid = (int)(nchunks < (uint64_t)num_sms() ? nchunks : (uint64_t)num_sms());
+      ProfScope prof_("select_stream", s);
+      k<<<grid, (1 + 2 * S) * 32, smem, s>>>(c, fp, bits, seg_info, ns_fast, mw, err, nullptr);
+    };
 #define MS_PICK(K)                                                                                   \
   do {                                                                                               \
-    if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow);          \
+    if (stream) pick_stream(select_stream_kernel<K == FAST_UNCOMPR ? FAST_STATIC : K, CORE_SELECT>);  \
+    else if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow>, 2, 4, kPairBufNarrow);     \
     else if (medium) pick(select_fast_kernel<K, 2, 4, 4, kPairBufMedium>, 2, 4, kPairBufMedium);     \
     else pick(select_fast_kernel<K, 2, 4, 3>, 2, 4);                                                 \
   } while (0)
@@ -410,9 +424,21 @@ cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err,
     ProfScope prof_("sum_fast", s);
     k<<<grid, 4 * 32, smem, s>>>(c, fp, nullptr, nullptr, ns_fast, spw, err, out);
   };
+  const uint32_t mw = kind == FAST_STATIC ? c.w : c.maxw;
+  const bool stream = kind != FAST_UNCOMPR && mw >= 1 && mw <= 32;
+  auto pick_stream = [&](auto k) {
+    const int S = ss_stages(mw);
+    const size_t smem = ss_smem_bytes(mw, S);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t nchunks = (ns_fast + kSsSegs - 1) / kSsSegs;
+    const int grid = (int)(nchunks < (uint64_t)num_sms() ? nchunks : (uint64_t)num_sms());
+    ProfScope prof_("sum_stream", s);
+    k<<<grid, (1 + 2 * S) * 32, smem, s>>>(c, fp, nullptr, nullptr, ns_fast, mw, err, out);
+  };
 #define MS_PICK_SUM(K)                                                                               \
   do {                                                                                               \
-    if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow, CORE_SUM>, kPairBufNarrow);      \
+    if (stream) pick_stream(select_stream_kernel<K == FAST_UNCOMPR ? FAST_STATIC : K, CORE_SUM>);     \
+    else if (narrow) pick(select_fast_kernel<K, 2, 4, 6, kPairBufNarrow, CORE_SUM>, kPairBufNarrow); \
     else pick(select_fast_kernel<K, 2, 4, 3, kPairBufWide, CORE_SUM>, kPairBufWide);                 \
   } while (0)
   if (kind == FAST_UNCOMPR) MS_PICK_SUM(FAST_UNCOMPR);
