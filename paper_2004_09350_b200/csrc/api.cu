@@ -749,11 +749,18 @@ ms_status ms_morph(const ms_ctx* ctx_, const ms_column* in, ms_fmt fmt, ms_colum
     const ColView v = view_of(in);
     ms_fmt f = fmt;
     if (f.format == MS_STATIC_BP && f.bit_width == 0) {
-      MS_TRY_CUDA(launch_delta_max(v, sc.at<unsigned long long>(o_meta + 8), err, ctx.s));
-      uint64_t h[2];
-      MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
-      MS_TRY(status_from_bits((uint32_t)h[0]));
-      f.bit_width = ebw_host(h[1]) ? ebw_host(h[1]) : 1;
+      // the width from the block headers when their bounds agree, else from a max pass
+      MS_TRY_CUDA(launch_delta_bounds(v, sc.at<unsigned long long>(o_meta + 16), ctx.s));
+      uint64_t h[4];
+      MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 4));
+      uint32_t wb = ebw_host(h[3]);
+      if (ebw_host(h[2]) != wb) {
+        MS_TRY_CUDA(launch_delta_max(v, sc.at<unsigned long long>(o_meta + 8), err, ctx.s));
+        MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
+        MS_TRY(status_from_bits((uint32_t)h[0]));
+        wb = ebw_host(h[1]);
+      }
+      f.bit_width = wb ? wb : 1;
     }
     const uint64_t words = f.format == MS_UNCOMPR ? n : words_for(n, f.bit_width);
     MS_TRY(alloc_column(ctx, out, f, n, words, 0));

@@ -275,6 +275,51 @@ cudaError_t run(const ColView& c, uint32_t ws, uint64_t* out, unsigned long long
 
 }  // namespace
 
+// Header bounds of a DELTA_BP column's maximum (for the auto width of a morph into
+// STATIC_BP): every block's first value ref[b] is a value (lower bound); its
+// values are at most ref[b] + (B - 1)(2^w_b - 1) unless that sum passes 2^64
+// (the differences wrap: no bound, 2^64 - 1); the remainder is exact. When
+// ebw(lower) == ebw(upper) the width is known without decoding a block.
+__global__ void delta_bounds_kernel(ColView c, unsigned long long* lohi) {
+  uint64_t lo = 0, hi = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < c.nb; b += stride) {
+    const uint64_t r = __ldg(c.ref + b);
+    const uint32_t w = __ldg(c.cw + b + 1) - __ldg(c.cw + b);
+    uint64_t u = ~0ull;
+    if (w < 64) {
+      const uint64_t step = (1ull << w) - 1;
+      const uint64_t m = (uint64_t)(c.B - 1);
+      if (step == 0 || m <= ~0ull / step) {
+        const uint64_t span = m * step;
+        if (r <= ~0ull - span) u = r + span;
+      }
+    }
+    lo = r > lo ? r : lo;
+    hi = u > hi ? u : hi;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.nrem; i += stride) {
+    const uint64_t v = __ldg(c.rem + i);
+    lo = v > lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  lo = warp_max(lo);
+  hi = warp_max(hi);
+  if ((threadIdx.x & 31) == 0) {
+    if (lo) atomicMax(lohi, (unsigned long long)lo);
+    if (hi) atomicMax(lohi + 1, (unsigned long long)hi);
+  }
+}
+
+cudaError_t launch_delta_bounds(const ColView& c, unsigned long long* lohi, cudaStream_t s) {
+  uint64_t grid = (c.nb + c.nrem + 255) / 256;
+  if (grid > (uint64_t)num_sms() * 8) grid = num_sms() * 8;
+  if (!grid) grid = 1;
+  ProfScope prof_("delta_bounds", s);
+  delta_bounds_kernel<<<(int)grid, 256, 0, s>>>(c, lohi);
+  return cudaGetLastError();
+}
+
 bool delta_direct_supported(const ColView& c) { return c.format == MS_DELTA_BP && c.B >= 128; }
 
 cudaError_t launch_delta_decode(const ColView& c, uint64_t* out, uint32_t* err, cudaStream_t s) {

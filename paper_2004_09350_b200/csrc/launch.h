@@ -164,6 +164,8 @@ cudaError_t launch_rle_write_col(const ColView& c, const uint64_t* first_last, c
 
 // DELTA_BP (B >= 128) decoded by lanes of 64 rows (delta.cu): into u64 values, its maximum, or a
 // static-BP stream at width ws (every payload word written; MS_E_WIDTH_OVERFLOW if a value needs more)
+// header bounds of a DELTA_BP column's maximum: lohi[0] = lower, lohi[1] = upper (zeroed by the caller)
+cudaError_t launch_delta_bounds(const ColView& c, unsigned long long* lohi, cudaStream_t s);
 bool delta_direct_supported(const ColView& c);
 cudaError_t launch_delta_decode(const ColView& c, uint64_t* out, uint32_t* err, cudaStream_t s);
 cudaError_t launch_delta_max(const ColView& c, unsigned long long* max_out, uint32_t* err, cudaStream_t s);

@@ -82,6 +82,37 @@ def test_morph_pairs(kind, rng):
                 assert_same_image(gm, O.morph(oa, *oracle_fmt(b)), f"morph {a}->{b} {kind} n={n}")
 
 
+@pytest.mark.parametrize("case", ["far", "near", "wrap", "zeros"])
+def test_morph_delta_to_static_auto_width(case):
+    """DELTA_BP -> STATIC_BP{auto}: the width comes from the block headers when the
+    bounds [max ref, max ref + (B-1)(2^w - 1)] share one effective width, else from a
+    max pass over the decoded values; both give the oracle's image (P:122 width of
+    the maximum). 'near': the maximum sits just under 2^30 so the bounds straddle it;
+    'wrap': differences that wrap mod 2^64 (no header bound)."""
+    ms = get_ms()
+    rng = np.random.default_rng(3)
+    n = 5 * 2048 + 77
+    if case == "far":
+        v = np.cumsum(rng.integers(0, 3, n)).astype(np.uint64) + np.uint64(1 << 29)
+    elif case == "near":
+        v = np.cumsum(rng.integers(0, 3, n)).astype(np.uint64)
+        v = v + np.uint64((1 << 30) - 5 - int(v[-1]))
+    elif case == "wrap":
+        v = rng.integers(0, 1 << 40, n).astype(np.uint64)
+    else:
+        v = np.zeros(n, np.uint64)
+    d = ms.compress(to_torch(v), ms.delta_bp(2048))
+    ms.profile_read()
+    ms.profile_enable(True)
+    try:
+        got = ms.morph(d, ms.static_bp(0))
+        names = set(ms.profile_read())
+    finally:
+        ms.profile_enable(False)
+    assert_same_image(got, O.morph(O.encode(v, O.DELTA_BP, 0, 2048), O.STATIC_BP, 0, 0), f"auto width {case}")
+    assert ("delta_max" in names) == (case in ("near", "wrap")), names
+
+
 @pytest.mark.parametrize("kind", ["small", "sorted", "runs", "outlier", "wide"])
 def test_many_tiles_per_cta(kind, rng):
     """More 2048-row tiles than resident CTAs (148 SMs x 4): the staged engine's
