@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "engine.cuh"
 #include "stage.cuh"
+#include "cstream.cuh"
 #include "grid.cuh"
 #include "launch.h"
 
@@ -134,6 +135,19 @@ static cudaError_t launch_staged(const ColView& src, const OutView& out, uint32_
 }
 
 cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s) {
+  // compress of u64 values into a block format, slot mode: warp-per-tile streamed encoder (cstream.cuh)
+  if (src.format == MS_UNCOMPR && out.slots && !out.n_dev && out.B >= 128 &&
+      (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP) &&
+      (reinterpret_cast<uintptr_t>(src.payload) & 15) == 0 && src.n == out.n) {
+    auto k = compress_stream_kernel;
+    const size_t smem = cs_smem_bytes();
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t tiles = (src.n + kChunk - 1) / kChunk;
+    const int grid = (int)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
+    ProfScope prof_("compress_stream", s);
+    k<<<grid, kCsThreads, smem, s>>>(src.payload, src.n, out, err);
+    return cudaGetLastError();
+  }
   // staged input (stage.cuh) whenever tiles go in a static order: every output but
   // a block format written with the look-back
   const bool ordered = !out.slots && (out.format == MS_DYN_BP || out.format == MS_FOR_BP || out.format == MS_DELTA_BP);
