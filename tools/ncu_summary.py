@@ -28,14 +28,14 @@ def main():
         agg = collections.defaultdict(lambda: [0, 0.0])
         # launches before the first select are the bench's setup (input generation and
         # compression of X and Y, outside the timed region): listed apart
-        started = not any("select_fast" in dict(zip(hdr, r)).get("Kernel Name", "") for r in rows)
+        started = not any(any(s in dict(zip(hdr, r)).get("Kernel Name", "") for s in ("select_fast", "select_stream")) for r in rows)
         for r in rows:
             x = dict(zip(hdr, r))
             if x.get("Metric Name") == "gpu__time_duration.sum":
                 unit = x["Metric Unit"]
                 v = float(x["Metric Value"].replace(",", ""))
                 v = v / 1e3 if unit == "ns" else v * 1e3 if unit == "ms" else v  # -> us
-                started = started or "select_fast" in x["Kernel Name"]
+                started = started or "select_fast" in x["Kernel Name"] or "select_stream" in x["Kernel Name"]
                 k = x["Kernel Name"].split("(")[0][:90] + ("" if started else " [setup]")
                 agg[k][0] += 1
                 agg[k][1] += v
