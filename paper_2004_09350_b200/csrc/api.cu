@@ -296,9 +296,15 @@ ms_status maybe_shrink(const Ctx& ctx, ms_column* out) {
 
 // Read back `count` u64 slots from device into host, synchronise, decode errors.
 ms_status readback(const Ctx& ctx, const uint64_t* dev, uint64_t* host, size_t count) {
-  if (count) MS_TRY_CUDA(cudaMemcpyAsync(host, dev, 8 * count, cudaMemcpyDeviceToHost, ctx.s));
+  uint64_t* pin = count && count <= 32 ? pinned_words() : nullptr;
+  if (pin) {
+    MS_TRY_CUDA(launch_readback(pin, dev, (uint32_t)count, nullptr, nullptr, nullptr, ctx.s));
+  } else if (count) {
+    MS_TRY_CUDA(cudaMemcpyAsync(host, dev, 8 * count, cudaMemcpyDeviceToHost, ctx.s));
+  }
   MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
   MS_TRY_CUDA(cudaGetLastError());
+  if (pin) std::memcpy(host, pin, 8 * count);
   return MS_OK;
 }
 
@@ -310,9 +316,7 @@ ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev,
   uint32_t maxw = 0;
   uint64_t maxw64 = 0;
   uint32_t* maxw_dev = nullptr;
-  if (is_block(out->fmt.format) && out->n_blocks && maxw_pre) {  // the width scan's maximum
-    MS_TRY_CUDA(cudaMemcpyAsync(&maxw64, maxw_pre, 8, cudaMemcpyDeviceToHost, ctx.s));
-  } else if (is_block(out->fmt.format) && out->n_blocks) {
+  if (is_block(out->fmt.format) && out->n_blocks && !maxw_pre) {
     maxw_dev = (uint32_t*)ctx.alloc(4);
     if (!maxw_dev) return MS_E_NOMEM;
     cudaError_t e = cudaMemsetAsync(maxw_dev, 0, 4, ctx.s);
@@ -323,10 +327,24 @@ ms_status finish_output(const Ctx& ctx, ms_column* out, const uint32_t* err_dev,
       return cuda_status(e);
     }
   }
-  MS_TRY_CUDA(cudaMemcpyAsync(&h[0], err_dev, 4, cudaMemcpyDeviceToHost, ctx.s));
-  if (is_block(out->fmt.format))
-    MS_TRY_CUDA(cudaMemcpyAsync(&h[1], out->cw + out->n_blocks, 4, cudaMemcpyDeviceToHost, ctx.s));
-  MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  uint64_t* pin = pinned_words();
+  if (pin && !maxw_dev) {  // one read-back kernel into pinned memory: err, cw[nb], the width scan's maximum
+    const bool mp = is_block(out->fmt.format) && out->n_blocks && maxw_pre;
+    MS_TRY_CUDA(launch_readback(pin, nullptr, 0, err_dev, is_block(out->fmt.format) ? out->cw + out->n_blocks : nullptr,
+                                mp ? maxw_pre : nullptr, ctx.s));
+    MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+    MS_TRY_CUDA(cudaGetLastError());
+    h[0] = pin[32];
+    h[1] = pin[33];
+    maxw64 = pin[34];
+  } else {
+    if (is_block(out->fmt.format) && out->n_blocks && maxw_pre)
+      MS_TRY_CUDA(cudaMemcpyAsync(&maxw64, maxw_pre, 8, cudaMemcpyDeviceToHost, ctx.s));
+    MS_TRY_CUDA(cudaMemcpyAsync(&h[0], err_dev, 4, cudaMemcpyDeviceToHost, ctx.s));
+    if (is_block(out->fmt.format))
+      MS_TRY_CUDA(cudaMemcpyAsync(&h[1], out->cw + out->n_blocks, 4, cudaMemcpyDeviceToHost, ctx.s));
+    MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+  }
   ctx.free(maxw_dev);
   MS_TRY_CUDA(cudaGetLastError());
   if (maxw_pre) maxw = (uint32_t)maxw64;

@@ -254,9 +254,9 @@ cudaError_t run(const ColView& c, uint32_t ws, uint64_t* out, unsigned long long
     const uint32_t stage_words = kDRows * mw / 64 + 2;
     const uint32_t out_words = MODE == DM_MAX ? 0u : (MODE == DM_U64 ? (uint32_t)kDRows : 32u * ws);
     const size_t smem = (size_t)kDWarps * (stage_words + out_words) * 8;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kDWarps * 32, smem);
+    per_sm = occupancy_cached((const void*)k, kDWarps * 32, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)per_sm * num_sms();
     const uint64_t need = ((main_rows + kDRows - 1) / kDRows + kDWarps - 1) / kDWarps;

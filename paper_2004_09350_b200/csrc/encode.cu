@@ -20,9 +20,9 @@ static cudaError_t run_warp_encode(const Src& src, const PosEnc& e0, uint64_t* s
     auto launch = [&](auto k) {
       const int warps = 4;
       const size_t smem = (size_t)warps * 2 * tile_slots(e.G) * 8;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set_smem_once((const void*)k, smem);
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+      per_sm = occupancy_cached((const void*)k, warps * 32, smem);
       if (per_sm < 1) per_sm = 1;
       uint64_t grid = (uint64_t)per_sm * num_sms();
       const uint64_t need = (n_items + warps - 1) / warps;
@@ -38,9 +38,9 @@ static cudaError_t run_warp_encode(const Src& src, const PosEnc& e0, uint64_t* s
   auto k = warp_encode_kernel<Src>;
   const int warps = e.G >= 2048 ? 2 : 4;
   const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_smem_once((const void*)k, smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+  per_sm = occupancy_cached((const void*)k, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)per_sm * num_sms();
   const uint64_t need = (n_items + warps - 1) / warps;
@@ -65,9 +65,9 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
   if (!n_items) return cudaSuccess;
   const uint64_t n_words = NS * kSegWords;
   auto grid_for = [&](auto k, size_t smem, uint64_t items) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPdWarps * 32, smem);
+    per_sm = occupancy_cached((const void*)k, kPdWarps * 32, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t g = (uint64_t)per_sm * num_sms();
     const uint64_t need = (items + kPdWarps - 1) / kPdWarps;
@@ -152,9 +152,9 @@ cudaError_t launch_semi_mask(const ColView& pos1, const ColView& keys, uint64_t 
   if (!n_items) return cudaSuccess;
   const int warps = 4;
   const size_t smem = (size_t)warps * tile_slots(kSegRows) * 8;
-  cudaFuncSetAttribute(semi_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_smem_once((const void*)semi_mask_kernel, smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, semi_mask_kernel, warps * 32, smem);
+  per_sm = occupancy_cached((const void*)semi_mask_kernel, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)per_sm * num_sms();
   const uint64_t need = (n_items + warps - 1) / warps;
@@ -178,9 +178,9 @@ cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64
   auto launch = [&](auto k) {
     const int warps = 4;
     const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+    per_sm = occupancy_cached((const void*)k, warps * 32, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)per_sm * num_sms();
     const uint64_t need = (n_items + warps - 1) / warps;
@@ -217,9 +217,9 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
   auto launch = [&](auto k, auto src) {
     const int warps = 4;
     const size_t smem = (size_t)warps * tile_slots(e.G) * 8;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32, smem);
+    per_sm = occupancy_cached((const void*)k, warps * 32, smem);
       if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)per_sm * num_sms();
     const uint64_t need = (n_items + warps - 1) / warps;
@@ -241,7 +241,7 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
     if (r != cudaSuccess) return r;
     auto k = project_stream_kernel<kPsStages, kPsPairs>;
     const size_t smem = ps_smem_bytes();
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     const uint64_t grid = n_items < (uint64_t)num_sms() ? n_items : (uint64_t)num_sms();
     ProfScope prof_("project_stream", s);
     k<<<(int)grid, kPsThreads, smem, s>>>(src, e, n_items, wins, slots, slot_words, wk, err);

@@ -14,6 +14,84 @@
 
 namespace ms {
 
+// ----------------------------------------------------------------- size read-backs
+// The few words an op reads back (sizes, error bits) are written by one small kernel
+// straight into pinned host memory, then the stream is synchronised: one launch
+// instead of several pageable device-to-host copies in the gap after each op.
+__global__ void readback_kernel(uint64_t* __restrict__ host, const uint64_t* __restrict__ dev, uint32_t count,
+                                const uint32_t* __restrict__ w0, const uint32_t* __restrict__ w1,
+                                const uint64_t* __restrict__ d2) {
+  const uint32_t t = threadIdx.x;
+  if (t < count) host[t] = dev[t];
+  if (t == 32) host[32] = w0 ? *w0 : 0u;
+  if (t == 33) host[33] = w1 ? *w1 : 0u;
+  if (t == 34) host[34] = d2 ? *d2 : 0ull;
+}
+
+uint64_t* pinned_words() {
+  thread_local uint64_t* p[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!p[dev] && cudaHostAlloc((void**)&p[dev], 64 * sizeof(uint64_t), cudaHostAllocPortable) != cudaSuccess)
+    p[dev] = nullptr;
+  return p[dev];
+}
+
+cudaError_t launch_readback(uint64_t* host, const uint64_t* dev, uint32_t count, const uint32_t* w0,
+                            const uint32_t* w1, const uint64_t* d2, cudaStream_t s) {
+  readback_kernel<<<1, 64, 0, s>>>(host, dev, count, w0, w1, d2);
+  count_launch();
+  return cudaGetLastError();
+}
+// ----------------------------------------------------------------- launch-config cache
+namespace {
+struct CfgKey {
+  int dev;
+  const void* k;
+  int threads;
+  size_t smem;
+  bool operator==(const CfgKey& o) const { return dev == o.dev && k == o.k && threads == o.threads && smem == o.smem; }
+};
+std::mutex g_cfg_mu;
+std::vector<std::pair<CfgKey, int>> g_occ;
+std::vector<std::pair<CfgKey, int>> g_smem;  // threads unused: the largest opt-in set so far
+}  // namespace
+
+void set_smem_once(const void* kernel, size_t smem) {
+  if (smem <= 48 * 1024) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_cfg_mu);
+  for (auto& e : g_smem)
+    if (e.first.dev == dev && e.first.k == kernel) {
+      if (e.first.smem >= smem) return;
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e.first.smem = smem;
+      return;
+    }
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  g_smem.push_back({CfgKey{dev, kernel, 0, smem}, 0});
+}
+
+int occupancy_cached(const void* kernel, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const CfgKey key{dev, kernel, threads, smem};
+  {
+    std::lock_guard<std::mutex> g(g_cfg_mu);
+    for (auto& e : g_occ)
+      if (e.first == key) return e.second;
+  }
+  set_smem_once(kernel, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  std::lock_guard<std::mutex> g(g_cfg_mu);
+  g_occ.push_back({key, per_sm});
+  return per_sm;
+}
+
+
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
@@ -123,7 +201,7 @@ static cudaError_t launch_staged(const ColView& src, const OutView& out, uint32_
     if (dev >= 0 && dev < 64) attr[dev][max_only] = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
+  per_sm = occupancy_cached((const void*)k, kThreads, dyn);
   if (per_sm < 1) per_sm = 1;
   const uint64_t items = n_items_hint(out);
   uint64_t g = (uint64_t)per_sm * num_sms();
@@ -141,7 +219,7 @@ cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* 
       (reinterpret_cast<uintptr_t>(src.payload) & 15) == 0 && src.n == out.n) {
     auto k = compress_stream_kernel;
     const size_t smem = cs_smem_bytes();
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     const uint64_t tiles = (src.n + kChunk - 1) / kChunk;
     const int grid = (int)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
     ProfScope prof_("compress_stream", s);

@@ -37,6 +37,16 @@ struct PredSpec {
   uint64_t bitmap_bits;
 };
 
+// launch-configuration queries cached per (device, kernel): the dynamic shared-memory
+// opt-in is set once per size, the occupancy computed once per (threads, smem) — both
+// are host round trips that otherwise sit in the gap after every size read-back
+void set_smem_once(const void* kernel, size_t smem);
+// pinned host words of this thread and device (64 u64; nullptr if cudaHostAlloc fails)
+uint64_t* pinned_words();
+// host[0..count) = dev[0..count) (count <= 32), host[32] = *w0, host[33] = *w1, host[34] = *d2 (null: 0)
+cudaError_t launch_readback(uint64_t* host, const uint64_t* dev, uint32_t count, const uint32_t* w0,
+                            const uint32_t* w1, const uint64_t* d2, cudaStream_t s);
+int occupancy_cached(const void* kernel, int threads, size_t smem);
 cudaError_t launch_engine_col(const ColView& src, const OutView& out, uint32_t* err, cudaStream_t s);
 cudaError_t launch_engine_bitmask(const uint32_t* bits, const uint64_t* tile_off, const uint32_t* start_tile,
                                   uint64_t n_words, uint64_t row_offset, const OutView& out, uint32_t* err,

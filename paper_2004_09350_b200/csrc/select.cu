@@ -263,9 +263,9 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
     FastPred fp{p.lo, p.span, p.neg, (uint32_t)p.is_bitmap, p.bitmap, p.bitmap_bits};
     auto pick = [&](auto k, int stages, int warps_per_cta, int bufu32 = kPairBufWide) {
       const size_t smem = (size_t)warps_per_cta * stages * bufu32 * 4;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set_smem_once((const void*)k, smem);
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps_per_cta * 32, smem);
+      per_sm = occupancy_cached((const void*)k, warps_per_cta * 32, smem);
       if (per_sm < 1) per_sm = 1;
       const uint64_t warps = (uint64_t)per_sm * num_sms() * warps_per_cta;
       uint64_t spw = (ns_fast + warps - 1) / warps;
@@ -286,7 +286,7 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
     auto pick_stream = [&](auto k) {
       const int S = ss_stages(mw);
       const size_t smem = ss_smem_bytes(mw, S);
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set_smem_once((const void*)k, smem);
       const uint64_t nchunks = (ns_fast + kSsSegs - 1) / kSsSegs;
       const int grid = (int)(nchunks < (uint64_t)num_sms() ? nchunks : (uint64_t)num_sms());
       ProfScope prof_("select_stream", s);
@@ -412,9 +412,9 @@ cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err,
   FastPred fp{};
   auto pick = [&](auto k, int bufu32) {
     const size_t smem = (size_t)4 * 2 * bufu32 * 4;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 4 * 32, smem);
+    per_sm = occupancy_cached((const void*)k, 4 * 32, smem);
     if (per_sm < 1) per_sm = 1;
     const uint64_t warps = (uint64_t)per_sm * num_sms() * 4;
     uint64_t spw = (ns_fast + warps - 1) / warps;
@@ -429,7 +429,7 @@ cudaError_t launch_sum(const ColView& c, unsigned long long* out, uint32_t* err,
   auto pick_stream = [&](auto k) {
     const int S = ss_stages(mw);
     const size_t smem = ss_smem_bytes(mw, S);
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)k, smem);
     const uint64_t nchunks = (ns_fast + kSsSegs - 1) / kSsSegs;
     const int grid = (int)(nchunks < (uint64_t)num_sms() ? nchunks : (uint64_t)num_sms());
     ProfScope prof_("sum_stream", s);
