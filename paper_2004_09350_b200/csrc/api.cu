@@ -551,9 +551,19 @@ ms_status positions_from_mask(const Ctx& ctx, uint32_t* bits, uint32_t* seg_info
                               sc.at<unsigned long long>(o_meta + 8), sc.at<uint64_t>(o_st1), sc.at<uint32_t>(o_tk1),
                               ctx.s));
   uint64_t h[4] = {0, 0, 0, 0};
-  if (NS) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], seg_off + NS, 8, cudaMemcpyDeviceToHost, ctx.s));
-  if (err_in) MS_TRY_CUDA(cudaMemcpyAsync(&h[3], err_in, 4, cudaMemcpyDeviceToHost, ctx.s));
-  MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
+  if (uint64_t* pin = pinned_words()) {  // the op's sizing read-back: one kernel into pinned memory
+    MS_TRY_CUDA(launch_readback(pin, sc.at<uint64_t>(o_meta), 2, err_in, nullptr, NS ? seg_off + NS : nullptr, ctx.s));
+    MS_TRY_CUDA(cudaStreamSynchronize(ctx.s));
+    MS_TRY_CUDA(cudaGetLastError());
+    h[0] = pin[0];
+    h[1] = pin[1];
+    h[2] = pin[34];
+    h[3] = pin[32];
+  } else {
+    if (NS) MS_TRY_CUDA(cudaMemcpyAsync(&h[2], seg_off + NS, 8, cudaMemcpyDeviceToHost, ctx.s));
+    if (err_in) MS_TRY_CUDA(cudaMemcpyAsync(&h[3], err_in, 4, cudaMemcpyDeviceToHost, ctx.s));
+    MS_TRY(readback(ctx, sc.at<uint64_t>(o_meta), h, 2));
+  }
   MS_TRY(status_from_bits((uint32_t)h[0] | (uint32_t)h[3]));
   const uint64_t n_out = NS ? h[2] : 0;
   const uint64_t max_pos = h[1] ? h[1] - 1 : 0;

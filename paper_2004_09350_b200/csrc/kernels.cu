@@ -442,19 +442,21 @@ struct NoKey {
 // select: segment offsets, 1 + max position, and the first position of every
 // output item (G ranks) that starts inside a segment (select-in-segment on the mask)
 struct SegEpi {
-  uint64_t* seg_off;
+  uint64_t* seg_off;  // only seg_off[NS] (the total) is written: the encoders start from gstart
   uint64_t* gstart;
   const uint32_t* seg_info;
   const uint32_t* bits;
   unsigned long long* max_pos1;  // 1 + largest selected position (0 if none)
   uint64_t row_offset;
   uint64_t NS;
-  uint32_t G;
+  uint32_t lgG;  // output item size G = 2^lgG
   __device__ void operator()(uint64_t idx, uint64_t off, uint64_t c) const {
-    seg_off[idx] = off;
     if (!c) return;
-    for (uint64_t k = (off + G - 1) / G; k * G < off + c; ++k) {
-      uint32_t q = (uint32_t)(k * G - off);  // rank inside the segment
+    const uint64_t G = 1ull << lgG;
+    uint64_t k = (off + G - 1) >> lgG;
+    if ((k << lgG) >= off + c) return;  // no output item starts in this segment
+    for (; (k << lgG) < off + c; ++k) {
+      uint32_t q = (uint32_t)((k << lgG) - off);  // rank inside the segment
       for (uint32_t wdi = 0; wdi < kSegWords; ++wdi) {
         const uint32_t word = bits[idx * kSegWords + wdi];
         const uint32_t pc = __popc(word);
@@ -477,7 +479,9 @@ struct SegEpi {
 cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint64_t NS, uint64_t row_offset,
                             uint32_t G, uint64_t* seg_off, uint64_t* gstart, unsigned long long* max_pos1,
                             uint64_t* status, uint32_t* ticket, cudaStream_t s) {
-  return run_scan(SegIn{seg_info}, SegEpi{seg_off, gstart, seg_info, bits, max_pos1, row_offset, NS, G}, NS, status,
+  uint32_t lg = 0;
+  while ((1u << lg) < G) ++lg;  // G is a power of two (block sizes 128..2048, or 512)
+  return run_scan(SegIn{seg_info}, SegEpi{seg_off, gstart, seg_info, bits, max_pos1, row_offset, NS, lg}, NS, status,
                   ticket, s);
 }
 
