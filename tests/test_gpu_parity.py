@@ -340,3 +340,32 @@ def test_max_width_hint(rng):
     gs = ms.select(c, ms.LT, 1 << 16, out_fmt=ms.delta_bp(512))
     assert_same_image(gs, O.select(O.encode(v, O.DYN_BP, 0, 512), O.LT, 1 << 16, out_fmt=O.DELTA_BP,
                                    out_block=512), "select with understated hint")
+
+
+@pytest.mark.parametrize("fname", ["dyn1024", "for2048", "static", "dyn512"])
+def test_select_stream_many_chunks(fname, rng):
+    """The CTA-streamed select / sum core (selstream.cuh) over more chunks per CTA
+    than stages (16 segments per chunk, 10 stages, 148 CTAs: > 12M rows), blocks
+    larger than a segment (B = 1024, 2048: segments inside a block), a static
+    width, a ragged tail of partial segments and the block remainder; images and
+    sums against the oracle."""
+    ms = get_ms()
+    n = (1 << 24) + 12_345
+    v = rng.integers(0, 1 << 19, n).astype(np.uint64)
+    v[rng.random(n) < 0.001] = np.uint64(1 << 21)  # some wider blocks
+    f = {"dyn1024": ms.dyn_bp(1024), "for2048": ms.for_bp(2048), "static": ms.static_bp(0),
+         "dyn512": ms.dyn_bp(512)}[fname]
+    gi = ms.compress(to_torch(v), f)
+    oi = O.encode(v, *oracle_fmt(f))
+    ms.profile_read()
+    ms.profile_enable(True)
+    try:
+        for op, a, b in ((ms.LT, 1 << 15, 0), (ms.BETWEEN, 1000, 1 << 18)):
+            gs = ms.select(gi, op, a, b, out_fmt=ms.delta_bp(512))
+            os_ = O.select(oi, oracle_op(op), a, b, out_fmt=O.DELTA_BP, out_block=512)
+            assert_same_image(gs, os_, f"select {f} {op}")
+        assert ms.u64(ms.agg_sum(gi)) == int(v.sum(dtype=np.uint64))
+        names = set(ms.profile_read())
+    finally:
+        ms.profile_enable(False)
+    assert "select_stream" in names and "sum_stream" in names, names
