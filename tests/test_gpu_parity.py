@@ -369,3 +369,23 @@ def test_select_stream_many_chunks(fname, rng):
     finally:
         ms.profile_enable(False)
     assert "select_stream" in names and "sum_stream" in names, names
+
+
+@pytest.mark.parametrize("kind", ["small", "sorted", "wide"])
+def test_compress_stream_stage_reuse(kind, rng):
+    """u64 -> DYN / FOR / DELTA_BP through the streamed compress (cstream.cuh) with
+    more 2048-row tiles per CTA than its 10 stages, every block size, a ragged
+    tail; byte-exact against the oracle."""
+    ms = get_ms()
+    n = (1 << 23) + 77
+    v = rand_values(n, kind, rng)
+    t = to_torch(v)
+    ms.profile_read()
+    ms.profile_enable(True)
+    try:
+        for f in (ms.dyn_bp(128), ms.for_bp(512), ms.delta_bp(2048), ms.delta_bp(256), ms.for_bp(1024)):
+            assert_same_image(ms.compress(t, f), O.encode(v, *oracle_fmt(f)), f"compress {f} {kind}")
+        names = set(ms.profile_read())
+    finally:
+        ms.profile_enable(False)
+    assert "compress_stream" in names

@@ -156,3 +156,20 @@ def test_project_stream_unsorted_and_range():
     with pytest.raises(ms.MsError) as e:
         ms.project(gd, ms.compress(to_torch(bad), ms.delta_bp(512)), 0, ms.for_bp(512))
     assert e.value.code == 4  # MS_E_RANGE
+
+
+def test_project_stream_stage_reuse():
+    """More output blocks per CTA than stages (7 stages x 148 CTAs): every stage
+    and consumer pair is reused many times; byte-exact against the oracle."""
+    ms = get_ms()
+    rng = np.random.default_rng(77)
+    n = 8_000_000 + 4321
+    v = _data(rng, n, "narrow")
+    sel = np.nonzero(rng.random(n) < 1 / 8)[0].astype(np.uint64)
+    gd = ms.compress(to_torch(v), ms.for_bp(512))
+    gp = ms.compress(to_torch(sel), ms.delta_bp(512))
+    assert gp.n // 512 > 7 * 148  # > 7 blocks per CTA
+    gr, names = _ran(ms, lambda: ms.project(gd, gp, 0, ms.for_bp(512)))
+    assert "project_stream" in names
+    assert_same_image(gr, O.project(O.encode(v, O.FOR_BP, 0, 512), O.encode(sel, O.DELTA_BP, 0, 512), 0,
+                                    O.FOR_BP, 0, 512), "stage reuse")
