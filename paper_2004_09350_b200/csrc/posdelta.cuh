@@ -14,10 +14,12 @@
 //              shared-memory copy of the block, stored with coalesced 64-bit
 //              stores at word cw[k] * B / 64; cw[k+1], base = p_0 = gstart[k].
 //              The final partial block goes raw to the remainder.
-// Per block the walk is pd_fast_item (mask span <= kPdStageU32 words, i.e.
-// selectivity above ~1.6%: words staged in shared memory, B/32 ranks per lane,
-// equal work per lane, 32-bit relative positions) or, for sparse masks, the
-// round-based walker pd_walk. No position is materialised outside registers.
+// Per block the walk is pd_item512 (B = 512, span < 512 words, i.e. selectivity
+// above ~3.1 %: words in registers, set bits scattered by rank into shared
+// memory, then 16 ranks per lane packed at a compile-time width),
+// pd_fast_item (span <= kPdStageU32 words: words staged in shared memory, B/32
+// ranks per lane located by a search) or, for sparse masks, the round-based
+// walker pd_walk. No position is materialised outside the SM.
 #pragma once
 #include "common.cuh"
 #include "launch.h"
@@ -283,6 +285,154 @@ __device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bi
   return pd_after_stage<PER, PACK, AUTO_W>(cnt, C, wa, w, stage, buf, lane);
 }
 
+// ---------------------------------------------------------------------------
+// B = 512 blocks whose mask span fits 16 words per lane (first word of the
+// block .. word of the next block's first position < 512 words, i.e. a
+// selectivity above ~3.1 %). Count-distributed instead of rank-distributed:
+//   1. lane j holds the 4G consecutive words [wa + 4Gj, +4G) in registers
+//      (G = span / 128 rounded up; words outside [row0, rowE) masked), counts
+//      their set bits; a warp scan gives the rank of the lane's first bit;
+//   2. each lane scatters its positions (u16, relative to word wa) into
+//      p16[rank] — one find-lowest / clear / store per set bit, no search;
+//   3. lane j reads ranks [16j, 16j + 16), d_q = p_q - p_{q-1} (d_0 = 0,
+//      D-6), w = ebw(max d) by a warp max, and packs its 16 codes at a
+//      compile-time width: its bits are exactly the halfwords [jw, jw + w)
+//      of the block (16w bits), so lanes never share a store.
+// The span bounds every relative row by 512 * 32, so d < 2^14 and w <= 14.
+template <int W>
+__device__ __forceinline__ void pd_pack16(const uint32_t (&d)[16], uint16_t* out, uint32_t lane) {
+  constexpr int NS = (16 * W + 31) / 32;
+  uint32_t s[NS + 1];
+#pragma unroll
+  for (int i = 0; i <= NS; ++i) s[i] = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int bit = q * W, wd = bit >> 5, sh = bit & 31;
+    s[wd] |= d[q] << sh;
+    if (sh + W > 32) s[wd + 1] |= d[q] >> (32 - sh);
+  }
+  if (W % 2 == 0) {
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(out) + lane * (W / 2);
+#pragma unroll
+    for (int i = 0; i < W / 2; ++i) o32[i] = s[i];
+  } else {
+    uint16_t* o = out + lane * W;
+#pragma unroll
+    for (int h = 0; h < W; ++h) o[h] = (uint16_t)(s[h >> 1] >> ((h & 1) * 16));
+  }
+}
+
+// Ranks [16j, 16j + 16) -> d, w = ebw(max d), the block packed into p16 (in place).
+__device__ __forceinline__ uint32_t pd_pack512(uint16_t* p16, uint32_t lane) {
+  const uint4 a = reinterpret_cast<const uint4*>(p16)[2 * lane];
+  const uint4 b = reinterpret_cast<const uint4*>(p16)[2 * lane + 1];
+  const uint32_t pw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  uint32_t p[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    p[2 * i] = pw[i] & 0xffffu;
+    p[2 * i + 1] = pw[i] >> 16;
+  }
+  const uint32_t prev = __shfl_up_sync(kFull, p[15], 1);
+  uint32_t d[16];
+  d[0] = lane ? p[0] - prev : 0u;
+  uint32_t mx = d[0];
+#pragma unroll
+  for (int q = 1; q < 16; ++q) {
+    d[q] = p[q] - p[q - 1];
+    mx = d[q] > mx ? d[q] : mx;
+  }
+  mx = __reduce_max_sync(kFull, mx);
+  const uint32_t w = 32u - __clz(mx);
+  __syncwarp();
+  switch (w) {
+    case 1: pd_pack16<1>(d, p16, lane); break;
+    case 2: pd_pack16<2>(d, p16, lane); break;
+    case 3: pd_pack16<3>(d, p16, lane); break;
+    case 4: pd_pack16<4>(d, p16, lane); break;
+    case 5: pd_pack16<5>(d, p16, lane); break;
+    case 6: pd_pack16<6>(d, p16, lane); break;
+    case 7: pd_pack16<7>(d, p16, lane); break;
+    case 8: pd_pack16<8>(d, p16, lane); break;
+    case 9: pd_pack16<9>(d, p16, lane); break;
+    case 10: pd_pack16<10>(d, p16, lane); break;
+    case 11: pd_pack16<11>(d, p16, lane); break;
+    case 12: pd_pack16<12>(d, p16, lane); break;
+    case 13: pd_pack16<13>(d, p16, lane); break;
+    case 14: pd_pack16<14>(d, p16, lane); break;
+    default: break;  // w == 0 cannot happen past rank 0: positions are distinct
+  }
+  __syncwarp();
+  return w;
+}
+
+// Steps 1-2 with C words per lane (compile time, so the words stay in
+// registers): lane j holds words [wi + Cj, wi + Cj + C) of the S-word span.
+template <int C>
+__device__ __forceinline__ bool pd_scatter512(const uint32_t* __restrict__ bits, uint64_t row0, uint64_t rowE,
+                                              uint16_t* p16, uint32_t lane) {
+  const uint64_t wi = row0 >> 5;
+  const uint32_t S = (uint32_t)((rowE >> 5) - wi) + 1u;
+  const uint32_t lmask = (1u << (rowE & 31)) - 1u;  // rows before the next block's first position
+  const uint32_t base = C * lane;
+  const uint32_t* src = bits + wi + base;
+  uint32_t x[C];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    uint32_t v = 0u;
+    if (base + i < S) v = __ldg(src + i);
+    if (base + i == S - 1) v &= lmask;
+    x[i] = v;
+  }
+  if (lane == 0) x[0] &= ~0u << (row0 & 31);
+#pragma unroll
+  for (int i = 0; i < C; ++i) cnt += __popc(x[i]);
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, inc, o);
+    if (lane >= (uint32_t)o) inc += t;
+  }
+  if (__shfl_sync(kFull, inc, 31) != 512u) return false;  // the scan's block start disagrees with the mask
+  // highest set bit first (one FLO per position, no bit reversal), from the
+  // lane's last rank down
+  uint32_t dst = (uint32_t)__cvta_generic_to_shared(p16 + inc - 1);  // the lane's last rank
+#pragma unroll
+  for (int i = C - 1; i >= 0; --i) {
+    uint32_t word = x[i];
+    const uint32_t rb = (base + i) * 32u;
+    while (word) {
+      uint32_t b, m;
+      asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(word));         // highest set bit
+      asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(m) : "r"(b));    // the bits below it
+      word &= m;
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)(rb + b)) : "memory");
+      dst -= 2;
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+__device__ __forceinline__ uint32_t pd_item512(const uint32_t* __restrict__ bits, uint64_t row0, uint64_t rowE,
+                                               uint16_t* p16, uint32_t lane, uint32_t* err) {
+  const uint32_t S = (uint32_t)((rowE >> 5) - (row0 >> 5)) + 1u;  // <= 512 (caller)
+  bool ok;
+  switch ((S + 31) / 32) {
+#define PD_C(c) case c: ok = pd_scatter512<c>(bits, row0, rowE, p16, lane); break;
+    PD_C(1) PD_C(2) PD_C(3) PD_C(4) PD_C(5) PD_C(6) PD_C(7) PD_C(8)
+    PD_C(9) PD_C(10) PD_C(11) PD_C(12) PD_C(13) PD_C(14) PD_C(15) PD_C(16)
+#undef PD_C
+    default: ok = false;
+  }
+  if (!ok) {
+    if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+    return 0u;
+  }
+  return pd_pack512(p16, lane);
+}
+
 __device__ __forceinline__ bool pd_span(const uint64_t* gstart, uint64_t item, uint64_t n_items, uint64_t row0,
                                         uint64_t row_offset, uint64_t* span) {
   if (item + 1 >= n_items) return false;  // the last block's span is unknown: walker
@@ -348,7 +498,7 @@ __global__ void __launch_bounds__(kPdWarps * 32) pos_pack_kernel(const uint32_t*
 // into cw; pos_copy moves each block from its slot to word cw[k] * B / 64. The
 // extra traffic (slots written and read back, ~2 x the positions image) costs
 // less than a second walk of the mask.
-__global__ void __launch_bounds__(kPdWarps * 32) pos_slot_kernel(const uint32_t* __restrict__ bits,
+__global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32_t* __restrict__ bits,
                                                                  uint64_t n_words,
                                                                  const uint64_t* __restrict__ gstart,
                                                                  uint64_t row_offset, PosEnc e, uint64_t n_items,
@@ -360,8 +510,17 @@ __global__ void __launch_bounds__(kPdWarps * 32) pos_slot_kernel(const uint32_t*
   const uint32_t B = e.G;
   const uint64_t n_full = e.n_out / B;
   const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
-  for (uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid; item < n_items; item += nwarps) {
-    const uint64_t row0 = __ldg(gstart + item) - row_offset;
+  uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid;
+  // the block's first position and the next block's, one item ahead (two dependent
+  // DRAM round trips per block otherwise: gstart, then the mask)
+  uint64_t g0 = 0, g1 = 0;
+  if (item < n_items) g0 = __ldg(gstart + item);
+  if (item + 1 < n_items) g1 = __ldg(gstart + item + 1);
+  for (; item < n_items; item += nwarps) {
+    const uint64_t row0 = g0 - row_offset, rowE = g1 - row_offset;
+    const uint64_t nx = item + nwarps;
+    if (nx < n_items) g0 = __ldg(gstart + nx);
+    if (nx + 1 < n_items) g1 = __ldg(gstart + nx + 1);
     if (item >= n_full) {  // final partial block -> raw remainder
       pd_walk<true>(bits, n_words, row0, (uint32_t)(e.n_out - item * B), 0, nullptr, e.rem, row_offset, lane, err);
       continue;
@@ -369,7 +528,10 @@ __global__ void __launch_bounds__(kPdWarps * 32) pos_slot_kernel(const uint32_t*
     uint64_t span;
     uint32_t w;
     const uint32_t* packed;
-    if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
+    if (B == 512 && item + 1 < n_items && (rowE >> 5) - (row0 >> 5) < 512) {
+      w = pd_item512(bits, row0, rowE, reinterpret_cast<uint16_t*>(stage), lane, err);
+      packed = stage;
+    } else if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
       uint32_t* buf = stage + kPdStageU32;
       w = B == 512   ? pd_fast_item<16, true, true>(bits, n_words, row0, span, 0, stage, buf, lane)
           : B == 256 ? pd_fast_item<8, true, true>(bits, n_words, row0, span, 0, stage, buf, lane)
@@ -384,13 +546,13 @@ __global__ void __launch_bounds__(kPdWarps * 32) pos_slot_kernel(const uint32_t*
       __syncwarp();
       packed = stage;
     }
-    const uint32_t nw64 = B / 64 * w;
-    if (nw64 > slot_words) {  // cannot happen: wcap bounds every delta
+    const uint32_t n16 = B / 128 * w;  // 16-byte units (B >= 128)
+    if (n16 * 2 > slot_words) {  // cannot happen: wcap bounds every delta
       if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
     } else {
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(packed);
-      uint64_t* dst = slots + item * slot_words;
-      for (uint32_t m = lane; m < nw64; m += 32) dst[m] = src[m];
+      const uint4* src = reinterpret_cast<const uint4*>(packed);
+      uint4* dst = reinterpret_cast<uint4*>(slots + item * slot_words);
+      for (uint32_t m = lane; m < n16; m += 32) dst[m] = src[m];
     }
     if (lane == 0) {
       wk[item] = w;

@@ -11,7 +11,7 @@ from tests.gpu_util import assert_same_image, get_ms, to_torch
 
 pytestmark = pytest.mark.gpu
 
-SELECTIVITY = [1.0, 0.9, 0.5, 0.0625, 0.02, 0.0155, 0.005, 0.0003]
+SELECTIVITY = [1.0, 0.9, 0.5, 0.125, 0.0625, 0.04, 0.031, 0.02, 0.0155, 0.005, 0.0003]
 
 
 @pytest.mark.parametrize("sel", SELECTIVITY)
