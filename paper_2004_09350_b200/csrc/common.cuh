@@ -245,9 +245,18 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, uint32_t m
 }
 
 // select-in-word: position of the (k+1)-th set bit of x (k < popc(x))
-__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
-  for (uint32_t i = 0; i < k; ++i) x &= x - 1;
-  return __ffs(x) - 1;
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {  // by halving: five popcounts
+  uint32_t pos = 0;
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1) {
+    const uint32_t c = __popc(x & ((1u << h) - 1u));
+    if (k >= c) {
+      k -= c;
+      x >>= h;
+      pos += h;
+    }
+  }
+  return pos;
 }
 
 // ---------------------------------------------------------- random access

@@ -278,6 +278,22 @@ cudaError_t launch_tile_copy(const OutView& o, uint64_t n_tiles, uint64_t nb, co
 // ----------------------------------------------------------- generic scan
 // Exclusive prefix over N values in one pass (decoupled look-back); epi(idx,
 // exclusive, value) consumes each entry, epi_total(total) is called once.
+// The epilogue's max key (select: 1 + largest position; widths: the largest) over
+// the CTA, then one atomicMax per CTA: a per-warp atomic on one address serialises
+// ~30K updates at L2 on a 2^32-row select.
+template <class Epi>
+__device__ __forceinline__ void cta_max_key(const Epi& epi, uint64_t key) {
+  __shared__ uint64_t red[kThreads / 32];
+  key = warp_max(key);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t m = 0;
+    for (int k = 0; k < kThreads / 32; ++k) m = red[k] > m ? red[k] : m;
+    if (m) epi.max_key(m);
+  }
+}
+
 template <class In, class Epi>
 __global__ void __launch_bounds__(kThreads) scan_kernel(In in, Epi epi, uint64_t N, uint64_t* status,
                                                         uint32_t* ticket) {
@@ -286,6 +302,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(In in, Epi epi, uint64_t
   __shared__ uint64_t s_E;
   const uint64_t n_items = (N + kChunk - 1) / kChunk;
   const int tid = threadIdx.x;
+  uint64_t key = 0;  // the largest key this thread saw: one atomic per CTA at the end
   while (true) {
     if (tid == 0) s_item = atomicAdd(ticket, 1u);
     __syncthreads();
@@ -307,7 +324,6 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(In in, Epi epi, uint64_t
     }
     __syncthreads();
     uint64_t off = s_E + ex;
-    uint64_t key = 0;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
       if (base + q < N) {
@@ -318,10 +334,9 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(In in, Epi epi, uint64_t
       }
       off += v[q];
     }
-    key = warp_max(key);
-    if ((tid & 31) == 0 && key) epi.max_key(key);
     __syncthreads();
   }
+  cta_max_key(epi, key);
 }
 
 // Reduce-then-scan (no look-back): tile sums, one CTA scans them in place, then
@@ -379,6 +394,7 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(In in, Epi epi, ui
   __shared__ uint64_t scan_sm[16];
   const uint64_t n_items = (N + kChunk - 1) / kChunk;
   const int tid = threadIdx.x;
+  uint64_t key = 0;  // the largest key this thread saw: one atomic per CTA at the end
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const uint64_t base = item * kChunk + tid * kVPT;
     uint64_t v[kVPT];
@@ -390,7 +406,6 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(In in, Epi epi, ui
     }
     const uint64_t ex = cta_excl_scan(tsum, scan_sm, nullptr);  // ends with a barrier
     uint64_t off = tile_off[item] + ex;
-    uint64_t key = 0;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
       if (base + q < N) {
@@ -401,9 +416,8 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(In in, Epi epi, ui
       }
       off += v[q];
     }
-    key = warp_max(key);
-    if ((tid & 31) == 0 && key) epi.max_key(key);
   }
+  cta_max_key(epi, key);
 }
 
 template <class In, class Epi>
@@ -439,6 +453,36 @@ struct NoKey {
   __device__ void max_key(uint64_t) const {}
 };
 
+// row (within its 512-row segment) of the set bit of rank q (q < the segment's
+// count): the segment's 16 mask words in four independent 16-byte loads, the word
+// by a popcount walk in registers, the bit by halving. Out of line: rare (one call
+// per output block) and register-heavy next to the scan's unrolled epilogue.
+__device__ __forceinline__ uint32_t seg_row_of_rank(const uint32_t* __restrict__ seg, uint32_t q) {
+  static_assert(kSegWords == 16, "segment = 16 mask words");
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(seg) + i);
+    w[4 * i] = t.x; w[4 * i + 1] = t.y; w[4 * i + 2] = t.z; w[4 * i + 3] = t.w;
+  }
+  uint32_t word = 0, wdi = 0;
+  bool found = false;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t pc = __popc(w[i]);
+    if (!found) {
+      if (q < pc) {
+        found = true;
+        word = w[i];
+        wdi = i;
+      } else {
+        q -= pc;
+      }
+    }
+  }
+  return wdi * 32 + select_bit(word, q);
+}
+
 // select: segment offsets, 1 + max position, and the first position of every
 // output item (G ranks) that starts inside a segment (select-in-segment on the mask)
 struct SegEpi {
@@ -455,18 +499,8 @@ struct SegEpi {
     const uint64_t G = 1ull << lgG;
     uint64_t k = (off + G - 1) >> lgG;
     if ((k << lgG) >= off + c) return;  // no output item starts in this segment
-    for (; (k << lgG) < off + c; ++k) {
-      uint32_t q = (uint32_t)((k << lgG) - off);  // rank inside the segment
-      for (uint32_t wdi = 0; wdi < kSegWords; ++wdi) {
-        const uint32_t word = bits[idx * kSegWords + wdi];
-        const uint32_t pc = __popc(word);
-        if (q < pc) {
-          gstart[k] = row_offset + idx * kSegRows + wdi * 32 + select_bit(word, q);
-          break;
-        }
-        q -= pc;
-      }
-    }
+    for (; (k << lgG) < off + c; ++k)
+      gstart[k] = row_offset + idx * kSegRows + seg_row_of_rank(bits + idx * kSegWords, (uint32_t)((k << lgG) - off));
   }
   __device__ uint64_t key(uint64_t idx) const {
     const uint32_t last = seg_info[idx] >> 16;
@@ -476,13 +510,100 @@ struct SegEpi {
   __device__ void total(uint64_t t) const { seg_off[NS] = t; }
 };
 
+// The segment scan's apply pass with the block starts deferred: a thread that
+// finds output blocks starting in its segments queues (k, segment, rank) in
+// shared memory; after the tile's offsets are known the whole CTA resolves the
+// queue, one block start per thread. Inline (SegEpi::operator()) every thread of
+// a warp would walk a segment's words whenever one lane has a start (~6 % of
+// the segments at BJ.c5, i.e. almost every warp, eight times per tile).
+constexpr int kSegQ = 2048;
+__global__ void __launch_bounds__(kThreads, 5) seg_apply_kernel(SegIn in, SegEpi epi, uint64_t N,
+                                                             const uint64_t* tile_off) {
+  __shared__ uint64_t scan_sm[16];
+  __shared__ uint64_t qk[kSegQ];
+  __shared__ uint32_t qr[kSegQ];  // segment within the tile (11 bits) << 16 | rank in the segment
+  __shared__ uint32_t q_n;
+  const uint64_t n_items = (N + kChunk - 1) / kChunk;
+  const int tid = threadIdx.x;
+  const uint64_t G = 1ull << epi.lgG;
+  if (tid == 0) q_n = 0;
+  uint64_t key = 0;
+  // the thread's 8 seg_info words (count | 1-based last row << 16), one tile ahead
+  auto load8 = [&](uint64_t item, uint32_t (&r)[kVPT]) {
+    const uint64_t base = item * kChunk + tid * kVPT;
+    if (item < n_items && base + kVPT <= N) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(in.p + base));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(in.p + base) + 1);
+      r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) r[q] = item < n_items && base + q < N ? __ldg(in.p + base + q) : 0u;
+    }
+  };
+  uint32_t nxt[kVPT];
+  load8(blockIdx.x, nxt);
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint64_t t0 = item * kChunk, base = t0 + tid * kVPT;
+    uint32_t info[kVPT];
+    uint64_t tsum = 0;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      info[q] = nxt[q];
+      tsum += info[q] & 0xffffu;
+    }
+    const uint64_t toff = tile_off[item];
+    load8(item + gridDim.x, nxt);
+    const uint64_t ex = cta_excl_scan(tsum, scan_sm, nullptr);  // ends with a barrier
+    uint64_t off = toff + ex;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      const uint64_t idx = base + q, c = info[q] & 0xffffu;
+      if (idx < N && c) {
+        for (uint64_t k = (off + G - 1) >> epi.lgG; (k << epi.lgG) < off + c; ++k) {
+          const uint32_t rank = (uint32_t)((k << epi.lgG) - off);
+          const uint32_t slot = atomicAdd(&q_n, 1u);
+          if (slot < (uint32_t)kSegQ) {
+            qk[slot] = k;
+            qr[slot] = (uint32_t)(idx - t0) << 16 | rank;
+          } else {  // queue full (block sizes < 512 at high selectivity): resolve here
+            epi.gstart[k] = epi.row_offset + idx * kSegRows + seg_row_of_rank(epi.bits + idx * kSegWords, rank);
+          }
+        }
+        key = epi.row_offset + idx * kSegRows + (info[q] >> 16);  // increasing in idx
+      }
+      if (idx == N - 1) epi.total(off + c);
+      off += c;
+    }
+    __syncthreads();
+    const uint32_t nq = q_n < (uint32_t)kSegQ ? q_n : (uint32_t)kSegQ;
+    for (uint32_t t = tid; t < nq; t += kThreads) {
+      const uint64_t idx = t0 + (qr[t] >> 16);
+      epi.gstart[qk[t]] =
+          epi.row_offset + idx * kSegRows + seg_row_of_rank(epi.bits + idx * kSegWords, qr[t] & 0xffffu);
+    }
+    __syncthreads();
+    if (tid == 0) q_n = 0;
+  }
+  cta_max_key(epi, key);
+}
+
 cudaError_t launch_seg_scan(const uint32_t* seg_info, const uint32_t* bits, uint64_t NS, uint64_t row_offset,
                             uint32_t G, uint64_t* seg_off, uint64_t* gstart, unsigned long long* max_pos1,
                             uint64_t* status, uint32_t* ticket, cudaStream_t s) {
   uint32_t lg = 0;
   while ((1u << lg) < G) ++lg;  // G is a power of two (block sizes 128..2048, or 512)
-  return run_scan(SegIn{seg_info}, SegEpi{seg_off, gstart, seg_info, bits, max_pos1, row_offset, NS, lg}, NS, status,
-                  ticket, s);
+  const SegIn in{seg_info};
+  const SegEpi epi{seg_off, gstart, seg_info, bits, max_pos1, row_offset, NS, lg};
+  const uint64_t T = (NS + kChunk - 1) / kChunk;
+  if (T <= 1) return run_scan(in, epi, NS, status, ticket, s);  // one tile: the single-pass kernel
+  ProfScope prof_("scan", s);
+  auto kr = scan_reduce_kernel<SegIn>;
+  kr<<<persistent_grid(kr, kThreads, T), kThreads, 0, s>>>(in, NS, status);
+  scan_tiles_kernel<<<1, 1024, 0, s>>>(status, T);
+  seg_apply_kernel<<<persistent_grid(seg_apply_kernel, kThreads, T), kThreads, 0, s>>>(in, epi, NS, status);
+  count_launch();
+  count_launch();
+  return cudaGetLastError();
 }
 
 // exclusive prefix into off[0..T), total into off[T], the largest count into off[T + 1]
