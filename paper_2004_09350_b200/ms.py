@@ -169,11 +169,32 @@ def _alloc_fns():
     return _native_alloc[1], _native_alloc[2]
 
 
-def _ctx(stream: Optional[torch.cuda.Stream] = None, flags: int = 0) -> _Ctx:
+_get_device = torch._C._cuda_getDevice
+_get_raw_stream = torch._C._cuda_getCurrentRawStream
+
+
+def _raw(stream=None) -> int:
+    """cudaStream_t of a torch stream, a raw handle, or (None) the current stream —
+    without building a torch.cuda.Stream object per call."""
     if stream is None:
-        stream = torch.cuda.current_stream()
-    a, f = _alloc_fns()
-    return _Ctx(stream=stream.cuda_stream, alloc=a, free=f, alloc_ctx=None, flags=flags)
+        return _get_raw_stream(_get_device())
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+_ctx_cache = {}
+
+
+def _ctx(stream=None, flags: int = 0) -> _Ctx:
+    raw = _raw(stream)
+    c = _ctx_cache.get((raw, flags))
+    if c is None:
+        a, f = _alloc_fns()
+        c = _Ctx(stream=raw, alloc=a, free=f, alloc_ctx=None, flags=flags)
+        if len(_ctx_cache) < 1024:
+            _ctx_cache[(raw, flags)] = c
+    return c
 
 
 def _check(rc: int, where: str):
@@ -200,24 +221,29 @@ class Column:
     stream first waits for an event recorded on each of them, so the memory is
     not handed out again while their kernels may still read it."""
 
-    def __init__(self, c: _Column, owned: bool = True, stream: Optional[torch.cuda.Stream] = None):
+    def __init__(self, c: _Column, owned: bool = True, stream=None):
         self._c = c
         self._owned = owned
-        self._stream = stream if stream is not None else torch.cuda.current_stream()
-        self._users = {}
+        self._sraw = _raw(stream)
+        self._sobj = stream if isinstance(stream, torch.cuda.Stream) else None
+        self._users = None  # raw handle -> torch stream of every other stream that read the column
 
-    def _used_on(self, stream: torch.cuda.Stream):
-        if stream.cuda_stream != self._stream.cuda_stream:
-            self._users[stream.cuda_stream] = stream
+    def _used_on(self, raw: int, stream):
+        if raw != self._sraw:
+            if self._users is None:
+                self._users = {}
+            self._users[raw] = stream if stream is not None else torch.cuda.current_stream()
 
     def __del__(self):
         try:
             if self._owned and self._c.alloc:
-                for s in self._users.values():
-                    ev = torch.cuda.Event()
-                    ev.record(s)
-                    self._stream.wait_event(ev)
-                _lib.ms_column_release(ctypes.byref(_ctx(self._stream)), ctypes.byref(self._c))
+                if self._users:
+                    home = self._sobj if self._sobj is not None else torch.cuda.ExternalStream(self._sraw)
+                    for s in self._users.values():
+                        ev = torch.cuda.Event()
+                        ev.record(s)
+                        home.wait_event(ev)
+                _lib.ms_column_release(ctypes.byref(_ctx(self._sraw)), ctypes.byref(self._c))
         except Exception:
             pass
 
@@ -286,17 +312,18 @@ class Column:
         return f"Column({self.fmt}, n={self.n}, bytes={self.footprint()})"
 
 
-def _stream_of(stream) -> torch.cuda.Stream:
-    return stream if stream is not None else torch.cuda.current_stream()
+def _stream_of(stream):
+    return stream if stream is not None else _raw(None)
 
 
 def _uses(stream, *cols):
-    """Record that an op on `stream` reads `cols` (see Column)."""
-    s = _stream_of(stream)
+    """Record that an op on `stream` reads `cols` (see Column); returns the stream
+    (its raw handle when None was given)."""
+    raw = _raw(stream)
     for c in cols:
         if c is not None:
-            c._used_on(s)
-    return s
+            c._used_on(raw, stream)
+    return stream if stream is not None else raw
 
 
 def _fmt(f) -> _Fmt:
