@@ -75,11 +75,23 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
   };
   if (slots && n_full) {  // single walk: slots, scan, copy
     const size_t smem = (size_t)kPdWarps * kPdWarpU32 * 4;
-    const int grid = grid_for(pos_slot_kernel, smem, n_items);
+    // dense: a mean mask span per block under 384 words (most blocks take pd_item512);
+    // the blocks it defers are walked by a second launch
+    const bool dense = e.G == 512 && n_words < 384 * n_full;
     {
       ProfScope prof_("pos_slot", s);
-      pos_slot_kernel<<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items, slots,
-                                                         slot_words, wk, err);
+      if (dense) {
+        const int grid = grid_for(pos_slot_kernel<kPdDense>, smem, n_items);
+        pos_slot_kernel<kPdDense><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items,
+                                                                   slots, slot_words, wk, err);
+        pos_slot_kernel<kPdDeferredOnly><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e,
+                                                                          n_items, slots, slot_words, wk, err);
+        count_launch();
+      } else {
+        const int grid = grid_for(pos_slot_kernel<kPdAll>, smem, n_items);
+        pos_slot_kernel<kPdAll><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items,
+                                                                 slots, slot_words, wk, err);
+      }
     }
     cudaError_t r = cudaGetLastError();
     if (r != cudaSuccess) return r;
@@ -91,10 +103,8 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
     return cudaGetLastError();
   }
   // no full block: the remainder alone (raw positions)
-  const size_t smem = (size_t)kPdWarps * kPdWarpU32 * 4;
-  const int grid = grid_for(pos_pack_kernel, smem, n_items);
-  ProfScope prof_("pos_pack", s);
-  pos_pack_kernel<<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items, cwx, err);
+  ProfScope prof_("pos_rem", s);
+  pos_rem_kernel<<<1, 32, 0, s>>>(bits, n_words, gstart, row_offset, e, err);
   return cudaGetLastError();
 }
 

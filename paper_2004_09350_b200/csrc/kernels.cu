@@ -395,17 +395,31 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(In in, Epi epi, ui
   const uint64_t n_items = (N + kChunk - 1) / kChunk;
   const int tid = threadIdx.x;
   uint64_t key = 0;  // the largest key this thread saw: one atomic per CTA at the end
+  // the thread's values one tile ahead: the tile's load round trip overlaps the
+  // previous tile's scan and epilogue
+  uint64_t nxt[kVPT];
+  {
+    const uint64_t b0 = (uint64_t)blockIdx.x * kChunk + tid * kVPT;
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) nxt[q] = b0 + q < N ? in(b0 + q) : 0;
+  }
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const uint64_t base = item * kChunk + tid * kVPT;
     uint64_t v[kVPT];
     uint64_t tsum = 0;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
-      v[q] = base + q < N ? in(base + q) : 0;
+      v[q] = nxt[q];
       tsum += v[q];
     }
+    const uint64_t toff = tile_off[item];
+    {
+      const uint64_t b1 = base + (uint64_t)gridDim.x * kChunk;
+#pragma unroll
+      for (int q = 0; q < kVPT; ++q) nxt[q] = b1 + q < N ? in(b1 + q) : 0;
+    }
     const uint64_t ex = cta_excl_scan(tsum, scan_sm, nullptr);  // ends with a barrier
-    uint64_t off = tile_off[item] + ex;
+    uint64_t off = toff + ex;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
       if (base + q < N) {

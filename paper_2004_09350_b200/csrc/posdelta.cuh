@@ -7,19 +7,17 @@
 // comes from the segment scan. Three launches, none of which waits on another
 // CTA (a look-back per block or per tile of blocks stalls whole CTAs on their
 // predecessors, measured 3x slower on B200):
-//   pos_width  one warp per block: w_k = ebw(max_j d_j), d_j = p_j - p_{j-1},
-//              d_0 = 0 (D-6);
+//   pos_slot   one warp per block: one walk of the block's mask span, d_j =
+//              p_j - p_{j-1}, d_0 = 0 (D-6), w_k = ebw(max_j d_j), the
+//              block packed in shared memory and stored to a fixed-size slot;
 //   scan       exclusive prefix of w_k -> cw (D-4), the generic scan kernel;
-//   pos_pack   one warp per block: the same walk, codes streamed into a
-//              shared-memory copy of the block, stored with coalesced 64-bit
-//              stores at word cw[k] * B / 64; cw[k+1], base = p_0 = gstart[k].
-//              The final partial block goes raw to the remainder.
-// Per block the walk is pd_item512 (B = 512, span < 512 words, i.e. selectivity
-// above ~3.1 %: words in registers, set bits scattered by rank into shared
-// memory, then 16 ranks per lane packed at a compile-time width),
-// pd_fast_item (span <= kPdStageU32 words: words staged in shared memory, B/32
-// ranks per lane located by a search) or, for sparse masks, the round-based
-// walker pd_walk. No position is materialised outside the SM.
+//   pos_copy   every block from its slot to word cw[k] * B / 64.
+// The final partial block goes raw to the remainder. Per block the walk
+// is pd_item512 (B = 512, span < 512 words, i.e. selectivity above ~3.1 %: words
+// in registers, set bits scattered by rank into shared memory, 16 ranks per lane
+// packed at a compile-time width) or pd_item_walk (everything else: rounds of
+// 512 words, the same scatter with u32 rows, a runtime-width pack). No position
+// is materialised outside the SM.
 #pragma once
 #include "common.cuh"
 #include "launch.h"
@@ -29,9 +27,7 @@ namespace ms {
 constexpr int kPdWarps = 8;  // warps per CTA (independent)
 constexpr int kPdLaneWords = 8;
 constexpr int kPdRoundWords = 32 * kPdLaneWords;
-constexpr uint32_t kPdStageU32 = 1024;      // mask words staged per warp (also a slow block's pack buffer: 2B u32)
-constexpr uint32_t kPdPackU32 = 16 * 16;    // a fast block: B/32 * w <= 16 * 15 u32
-constexpr uint32_t kPdWarpU32 = kPdStageU32 + kPdPackU32;
+constexpr uint32_t kPdWarpU32 = 1024;  // shared memory per warp: a block of B <= 512 codes at w <= 64 bits
 
 // One walk over the mask for output block `item`: ranks [0, cnt) starting at
 // relative row row0. PACK = false: returns the lane's max delta. PACK = true:
@@ -147,142 +143,6 @@ __device__ __forceinline__ uint64_t pd_walk(const uint32_t* __restrict__ bits, u
     wb += kPdRoundWords;
   }
   return maxd;
-}
-
-// Fast block walk, for blocks whose mask span (first word of this block to the
-// word of the next block's first position) fits the stage: lane j owns the
-// PER = B/32 consecutive ranks [PER*j, PER*j + PER).
-//   1. lane j loads C consecutive words [wa + C*j, +C) (16-byte loads), masks
-//      the rows before the block's first position, stages them in shared
-//      memory and counts their set bits; warp exclusive scan -> rank of each
-//      lane's chunk;
-//   2. lane j finds the chunk holding rank PER*j (binary search over the chunk
-//      prefixes by shuffles), walks to its word and bit, then extracts PER
-//      positions in order (32-bit, relative to word wa);
-//   3. d_q = p_q - p_{q-1} (d_0 of lane j from lane j-1's last position, 0
-//      for rank 0). The span bounds every delta by 32 * kPdStageU32 < 2^15.
-// PACK = false: returns w = ebw(max d). PACK = true: streams lane j's codes —
-// (AUTO_W: at the width it computes; else at the given w) —
-// the contiguous bit range [PER*j*w, PER*(j+1)*w) — into buf (B*w/32 u32,
-// zeroed here): plain stores inside the range, atomicOr on the two words it
-// may share with its neighbours; returns w.
-template <int PER, bool PACK, bool AUTO_W>
-__device__ __forceinline__ uint32_t pd_after_stage(uint32_t cnt, uint32_t C, uint64_t wa, uint32_t w,
-                                                   const uint32_t* stage, uint32_t* buf, uint32_t lane) {
-  uint32_t inc = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(kFull, inc, o);
-    if (lane >= (uint32_t)o) inc += t;
-  }
-  const uint32_t ex = inc - cnt;
-  // 2. locate rank PER*j: the last lane L with ex_L <= r
-  const uint32_t r = PER * lane;
-  uint32_t L = 0;
-#pragma unroll
-  for (int step = 16; step > 0; step >>= 1) {
-    const uint32_t cand = L + step;
-    const uint32_t exc = __shfl_sync(kFull, ex, cand & 31);
-    if (cand < 32 && exc <= r) L = cand;
-  }
-  uint32_t skip = r - __shfl_sync(kFull, ex, L);
-  uint32_t m = C * L;  // staged word index
-  uint32_t cur = stage[m];
-  while (true) {
-    const uint32_t pc = __popc(cur);
-    if (skip < pc) break;
-    skip -= pc;
-    cur = stage[++m];
-  }
-  for (; skip; --skip) cur &= cur - 1;
-  uint32_t pos[PER];
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    while (!cur) cur = stage[++m];
-    pos[q] = m * 32 + (__ffs(cur) - 1);
-    cur &= cur - 1;
-  }
-  // 3. deltas
-  const uint32_t prev_last = __shfl_up_sync(kFull, pos[PER - 1], 1);
-  uint32_t d[PER];
-#pragma unroll
-  for (int q = 0; q < PER; ++q) d[q] = q ? pos[q] - pos[q - 1] : (lane ? pos[0] - prev_last : 0u);
-  if (!PACK || AUTO_W) {
-    uint32_t mx = 0;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) mx = d[q] > mx ? d[q] : mx;
-    mx = __reduce_max_sync(kFull, mx);
-    w = 32 - __clz(mx);
-    if (!PACK) return w;
-  }
-  // 4. pack (w <= 15)
-  const uint32_t nw32 = PER * w;  // == B * w / 32
-  for (uint32_t i = lane; i < nw32; i += 32) buf[i] = 0;
-  __syncwarp();
-  if (w) {
-    const uint32_t o = PER * lane * w;
-    uint32_t widx = o >> 5, nb = o & 31;
-    uint32_t acc = 0;
-    bool first = true;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      acc |= d[q] << nb;
-      nb += w;
-      if (nb >= 32) {
-        if (first) {
-          atomicOr(buf + widx, acc);
-          first = false;
-        } else {
-          buf[widx] = acc;
-        }
-        ++widx;
-        nb -= 32;
-        acc = nb ? d[q] >> (w - nb) : 0u;
-      }
-    }
-    if (nb) atomicOr(buf + widx, acc);
-  }
-  __syncwarp();
-  return w;
-}
-
-template <int PER, bool PACK, bool AUTO_W = false>
-__device__ __forceinline__ uint32_t pd_fast_item(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
-                                                 uint64_t span_words, uint32_t w, uint32_t* stage, uint32_t* buf,
-                                                 uint32_t lane) {
-  const uint64_t wi = row0 >> 5;
-  const uint32_t fmask = ~0u << (row0 & 31);
-  const uint64_t wa = wi & ~3ull;
-  const uint32_t need = (uint32_t)((wi - wa) + span_words);
-  const uint32_t C = ((need + 127) / 128) * 4;  // words per lane, multiple of 4, 32*C >= need
-  const uint32_t wi_rel = (uint32_t)(wi - wa);
-  // 1. stage + count
-  const uint64_t c0 = wa + (uint64_t)C * lane;
-  uint4* st4 = reinterpret_cast<uint4*>(stage) + (C / 4) * lane;
-  uint32_t cnt = 0;
-  for (uint32_t q = 0; q < C; q += 4) {
-    const uint64_t m = c0 + q;
-    uint32_t x0, x1, x2, x3;
-    if (m + 4 <= n_words) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4*>(bits + m));
-      x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w;
-    } else {
-      x0 = m < n_words ? __ldg(bits + m) : 0u;
-      x1 = m + 1 < n_words ? __ldg(bits + m + 1) : 0u;
-      x2 = m + 2 < n_words ? __ldg(bits + m + 2) : 0u;
-      x3 = 0u;
-    }
-    if (m == wa) {  // the first four words hold the block start (wi - wa < 4)
-      x0 = wi_rel > 0 ? 0u : x0 & fmask;
-      x1 = wi_rel > 1 ? 0u : (wi_rel == 1 ? x1 & fmask : x1);
-      x2 = wi_rel > 2 ? 0u : (wi_rel == 2 ? x2 & fmask : x2);
-      x3 = wi_rel == 3 ? x3 & fmask : x3;
-    }
-    st4[q / 4] = make_uint4(x0, x1, x2, x3);
-    cnt += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
-  }
-  __syncwarp();
-  return pd_after_stage<PER, PACK, AUTO_W>(cnt, C, wa, w, stage, buf, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -433,84 +293,208 @@ __device__ __forceinline__ uint32_t pd_item512(const uint32_t* __restrict__ bits
   return pd_pack512(p16, lane);
 }
 
-__device__ __forceinline__ bool pd_span(const uint64_t* gstart, uint64_t item, uint64_t n_items, uint64_t row0,
-                                        uint64_t row_offset, uint64_t* span) {
-  if (item + 1 >= n_items) return false;  // the last block's span is unknown: walker
-  *span = ((__ldg(gstart + item + 1) - row_offset) >> 5) - (row0 >> 5) + 1;
-  return *span + 4 <= kPdStageU32;
-}
 
-// A walk that packs every block at cw[k] = cwx[k] (exclusive prefix of the widths);
-// launched for outputs without a full block, where it writes the raw remainder.
-__global__ void __launch_bounds__(kPdWarps * 32) pos_pack_kernel(const uint32_t* __restrict__ bits,
-                                                                 uint64_t n_words,
-                                                                 const uint64_t* __restrict__ gstart,
-                                                                 uint64_t row_offset, PosEnc e, uint64_t n_items,
-                                                                 const uint64_t* __restrict__ cwx, uint32_t* err) {
-  extern __shared__ __align__(16) uint32_t pd_sm[];  // per warp: stage | fast pack buffer
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t* stage = pd_sm + (size_t)wid * kPdWarpU32;
-  const uint32_t B = e.G;
-  const uint64_t n_full = e.n_out / B;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
-  for (uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid; item < n_items; item += nwarps) {
-    const uint64_t row0 = __ldg(gstart + item) - row_offset;
-    if (item >= n_full) {  // final partial block -> raw remainder
-      pd_walk<true>(bits, n_words, row0, (uint32_t)(e.n_out - item * B), 0, nullptr, e.rem, row_offset, lane, err);
-      continue;
+// Single-pass walk for the other full blocks (sparser masks, B < 512, the block
+// before the last): rounds of 512 words (16 per lane, 16-byte loads), set bits
+// scattered by rank into p32 (u32 rows relative to word wa) until B are found;
+// then lane j reads ranks [PER*j, PER*j + PER), d_q = p_q - p_{q-1}, w = ebw(max d)
+// (<= 32), and streams its codes — the bit range [PER*j*w, PER*(j+1)*w) — into
+// the block buffer (zeroed; atomicOr on the two words a lane may share).
+// Returns false when the block spans 2^32 rows or more (relative rows would
+// wrap): the caller falls back to the two-walk pd_walk.
+template <int PER>
+__device__ __forceinline__ bool pd_item_walk(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
+                                             uint32_t* p32, uint32_t lane, uint32_t* err, uint32_t* w_out) {
+  constexpr uint32_t B = PER * 32;
+  constexpr uint32_t kRoundWords = 512;
+  const uint64_t wi = row0 >> 5, wa = wi & ~3ull;
+  const uint32_t fmask = ~0u << (row0 & 31);
+  uint32_t got = 0;
+  for (uint64_t wb = wa; got < B; wb += kRoundWords) {
+    if (wb >= n_words) {  // fewer set bits than the scan counted
+      if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+      *w_out = 0;
+      return true;
     }
-    const uint64_t E = __ldg(cwx + item);
-    const uint32_t w = (uint32_t)(__ldg(cwx + item + 1) - E);
-    uint64_t span;
-    const uint32_t* packed;
-    if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
-      uint32_t* buf = stage + kPdStageU32;
-      if (B == 512) pd_fast_item<16, true>(bits, n_words, row0, span, w, stage, buf, lane);
-      else if (B == 256) pd_fast_item<8, true>(bits, n_words, row0, span, w, stage, buf, lane);
-      else pd_fast_item<4, true>(bits, n_words, row0, span, w, stage, buf, lane);
-      packed = buf;
+    if ((wb - wa + kRoundWords) * 32 > 0xffffffffull) return false;
+    const uint64_t wl = wb + 16ull * lane;
+    uint32_t x[16];
+    if (wl + 16 <= n_words) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(bits + wl) + g);
+        x[4 * g] = v.x; x[4 * g + 1] = v.y; x[4 * g + 2] = v.z; x[4 * g + 3] = v.w;
+      }
     } else {
-      const uint32_t nw32 = B / 32 * w;
-      for (uint32_t m = lane; m < nw32; m += 32) stage[m] = 0;
-      __syncwarp();
-      if (w) pd_walk<true>(bits, n_words, row0, B, w, stage, nullptr, row_offset, lane, err);
-      __syncwarp();
-      packed = stage;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = wl + i < n_words ? __ldg(bits + wl + i) : 0u;
     }
-    if (lane == 0) {
-      if (E + w > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
-      e.cw[item + 1] = (uint32_t)(E + w);
-      e.ref[item] = row0 + row_offset;
+    if (wl == wa) {  // lane 0 of the first round holds the block's first word (wi - wa < 4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (wa + i < wi) x[i] = 0u;
+        else if (wa + i == wi) x[i] &= fmask;
+      }
     }
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(packed);
-    uint64_t* dst = e.payload + E * (B / 64);
-    const uint32_t nw64 = B / 64 * w;
-    for (uint32_t m = lane; m < nw64; m += 32) dst[m] = src[m];
-    __syncwarp();
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cnt += __popc(x[i]);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, inc, o);
+      if (lane >= (uint32_t)o) inc += t;
+    }
+    uint32_t r = got + inc - cnt;
+    if (r < B) {
+      const uint32_t rb = (uint32_t)(wl - wa) * 32u;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint32_t word = x[i];
+        while (word && r < B) {
+          p32[r++] = rb + 32u * i + (__ffs(word) - 1);
+          word &= word - 1u;
+        }
+      }
+    }
+    got += __shfl_sync(kFull, inc, 31);
   }
+  __syncwarp();
+  uint32_t d[PER];  // the positions, then (in place, last first) their deltas
+#pragma unroll
+  for (int q = 0; q < PER; ++q) d[q] = p32[PER * lane + q];
+  const uint32_t prev = __shfl_up_sync(kFull, d[PER - 1], 1);
+  uint32_t mx = 0;
+#pragma unroll
+  for (int q = PER - 1; q >= 0; --q) {
+    d[q] = q ? d[q] - d[q - 1] : (lane ? d[0] - prev : 0u);
+    mx = d[q] > mx ? d[q] : mx;
+  }
+  mx = __reduce_max_sync(kFull, mx);
+  const uint32_t w = 32u - __clz(mx);
+  __syncwarp();
+  const uint32_t nw32 = PER * w;  // == B * w / 32
+  for (uint32_t i = lane; i < nw32; i += 32) p32[i] = 0u;
+  __syncwarp();
+  if (w) {
+    const uint32_t o = PER * lane * w;
+    uint32_t widx = o >> 5, nb = o & 31;
+    uint64_t acc = 0;
+    bool first = true;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      acc |= (uint64_t)d[q] << nb;
+      nb += w;
+      if (nb >= 32) {
+        if (first) {
+          atomicOr(p32 + widx, (uint32_t)acc);
+          first = false;
+        } else {
+          p32[widx] = (uint32_t)acc;
+        }
+        ++widx;
+        nb -= 32;
+        acc >>= 32;
+      }
+    }
+    if (nb) atomicOr(p32 + widx, (uint32_t)acc);
+  }
+  __syncwarp();
+  *w_out = w;
+  return true;
 }
 
+// Outputs without a full block: the remainder alone, raw positions.
+__global__ void __launch_bounds__(kPdWarps * 32) pos_rem_kernel(const uint32_t* __restrict__ bits, uint64_t n_words,
+                                                                const uint64_t* __restrict__ gstart,
+                                                                uint64_t row_offset, PosEnc e, uint32_t* err) {
+  if (threadIdx.x >= 32) return;
+  const uint64_t row0 = __ldg(gstart) - row_offset;
+  pd_walk<true>(bits, n_words, row0, (uint32_t)e.n_out, 0, nullptr, e.rem, row_offset, threadIdx.x, err);
+}
 
 // ---------------------------------------------------------------------------
-// Single-walk variant (the default): pos_slot packs every full block at its own
-// width into a fixed-size slot (B * wcap bits, wcap = ebw(rows - 1) bounds
-// every delta) and records w_k and the base; the generic scan turns the widths
-// into cw; pos_copy moves each block from its slot to word cw[k] * B / 64. The
-// extra traffic (slots written and read back, ~2 x the positions image) costs
-// less than a second walk of the mask.
+// pos_slot packs every full block at its own width into a fixed-size slot
+// (B * wcap bits, wcap = ebw(rows - 1) bounds every delta) and records w_k and
+// the base; the generic scan turns the widths into cw; pos_copy moves each
+// block from its slot to word cw[k] * B / 64. The extra traffic (slots written
+// and read back, ~2 x the positions image) costs less than a second walk of the
+// mask. One warp per block, kPdWarpU32 words of shared memory per warp.
+// A packed block (stage, B*w bits) to its slot, its width and base.
+__device__ __forceinline__ void pd_store_slot(uint64_t item, uint32_t w, uint64_t base, const PosEnc& e,
+                                              uint64_t* slots, uint32_t slot_words, uint32_t* wk,
+                                              const uint32_t* stage, uint32_t lane, uint32_t* err) {
+  const uint32_t n16 = e.G / 128 * w;  // 16-byte units (B >= 128)
+  if (n16 * 2 > slot_words) {  // cannot happen: wcap bounds every delta
+    if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
+  } else {
+    const uint4* src = reinterpret_cast<const uint4*>(stage);
+    uint4* dst = reinterpret_cast<uint4*>(slots + item * slot_words);
+    for (uint32_t m = lane; m < n16; m += 32) dst[m] = src[m];
+  }
+  if (lane == 0) {
+    wk[item] = w;
+    e.ref[item] = base;
+  }
+  __syncwarp();
+}
+
+// MODE kPdDense (B = 512, mean span < 384 words): pd_item512 only; a block whose
+// span does not fit (and the block before the last) is marked kPdDeferred in wk
+// and left to a kPdDeferredOnly launch, which walks only the marked blocks. The
+// walk's registers stay out of the fast path. kPdAll: the walk for every block.
+constexpr int kPdAll = 0, kPdDense = 1, kPdDeferredOnly = 2;
+constexpr uint32_t kPdDeferred = 0xffffffffu;
+
+// One full block by the walk (pd_item_walk; two walks past 2^32 rows) into its slot.
+__device__ __forceinline__ void pd_walk_block(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
+                                              uint64_t item, uint64_t row_offset, const PosEnc& e, uint64_t* slots,
+                                              uint32_t slot_words, uint32_t* wk, uint32_t* stage, uint32_t lane,
+                                              uint32_t* err) {
+  const uint32_t B = e.G;
+  uint32_t w = 0;
+  const bool done = B == 512   ? pd_item_walk<16>(bits, n_words, row0, stage, lane, err, &w)
+                    : B == 256 ? pd_item_walk<8>(bits, n_words, row0, stage, lane, err, &w)
+                               : pd_item_walk<4>(bits, n_words, row0, stage, lane, err, &w);
+  if (!done) {  // a block spanning >= 2^32 rows: two walks, codes up to 64 bits
+    w = ebw64(warp_max(pd_walk<false>(bits, n_words, row0, B, 0, nullptr, nullptr, row_offset, lane, err)));
+    const uint32_t nw32 = B / 32 * w;
+    for (uint32_t m = lane; m < nw32; m += 32) stage[m] = 0;
+    __syncwarp();
+    if (w) pd_walk<true>(bits, n_words, row0, B, w, stage, nullptr, row_offset, lane, err);
+    __syncwarp();
+  }
+  pd_store_slot(item, w, row0 + row_offset, e, slots, slot_words, wk, stage, lane, err);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32_t* __restrict__ bits,
                                                                  uint64_t n_words,
                                                                  const uint64_t* __restrict__ gstart,
                                                                  uint64_t row_offset, PosEnc e, uint64_t n_items,
                                                                  uint64_t* __restrict__ slots, uint32_t slot_words,
                                                                  uint32_t* __restrict__ wk, uint32_t* err) {
-  extern __shared__ __align__(16) uint32_t pd_sm[];  // per warp: stage | fast pack buffer
+  extern __shared__ __align__(16) uint32_t pd_sm[];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* stage = pd_sm + (size_t)wid * kPdWarpU32;
   const uint32_t B = e.G;
   const uint64_t n_full = e.n_out / B;
   const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
-  uint64_t item = (uint64_t)blockIdx.x * kPdWarps + wid;
+  const uint64_t gw = (uint64_t)blockIdx.x * kPdWarps + wid;
+  if (MODE == kPdDeferredOnly) {  // the marked blocks: 32 wk words per warp step, a ballot
+    for (uint64_t b0 = gw * 32; b0 < n_full; b0 += nwarps * 32) {
+      const uint64_t it = b0 + lane;
+      uint32_t m = __ballot_sync(kFull, it < n_full && __ldg(wk + it) == kPdDeferred);
+      while (m) {
+        const uint64_t item = b0 + (__ffs(m) - 1);
+        m &= m - 1;
+        pd_walk_block(bits, n_words, __ldg(gstart + item) - row_offset, item, row_offset, e, slots, slot_words, wk,
+                      stage, lane, err);
+      }
+    }
+    return;
+  }
+  uint64_t item = gw;
   // the block's first position and the next block's, one item ahead (two dependent
   // DRAM round trips per block otherwise: gstart, then the mask)
   uint64_t g0 = 0, g1 = 0;
@@ -525,40 +509,17 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
       pd_walk<true>(bits, n_words, row0, (uint32_t)(e.n_out - item * B), 0, nullptr, e.rem, row_offset, lane, err);
       continue;
     }
-    uint64_t span;
-    uint32_t w;
-    const uint32_t* packed;
-    if (B == 512 && item + 1 < n_items && (rowE >> 5) - (row0 >> 5) < 512) {
-      w = pd_item512(bits, row0, rowE, reinterpret_cast<uint16_t*>(stage), lane, err);
-      packed = stage;
-    } else if (pd_span(gstart, item, n_items, row0, row_offset, &span)) {
-      uint32_t* buf = stage + kPdStageU32;
-      w = B == 512   ? pd_fast_item<16, true, true>(bits, n_words, row0, span, 0, stage, buf, lane)
-          : B == 256 ? pd_fast_item<8, true, true>(bits, n_words, row0, span, 0, stage, buf, lane)
-                     : pd_fast_item<4, true, true>(bits, n_words, row0, span, 0, stage, buf, lane);
-      packed = buf;
+    if (MODE == kPdDense) {
+      if (item + 1 < n_items && (rowE >> 5) - (row0 >> 5) < 512) {
+        const uint32_t w = pd_item512(bits, row0, rowE, reinterpret_cast<uint16_t*>(stage), lane, err);
+        pd_store_slot(item, w, row0 + row_offset, e, slots, slot_words, wk, stage, lane, err);
+      } else {
+        if (lane == 0) wk[item] = kPdDeferred;
+        __syncwarp();
+      }
     } else {
-      w = ebw64(warp_max(pd_walk<false>(bits, n_words, row0, B, 0, nullptr, nullptr, row_offset, lane, err)));
-      const uint32_t nw32 = B / 32 * w;
-      for (uint32_t m = lane; m < nw32; m += 32) stage[m] = 0;
-      __syncwarp();
-      if (w) pd_walk<true>(bits, n_words, row0, B, w, stage, nullptr, row_offset, lane, err);
-      __syncwarp();
-      packed = stage;
+      pd_walk_block(bits, n_words, row0, item, row_offset, e, slots, slot_words, wk, stage, lane, err);
     }
-    const uint32_t n16 = B / 128 * w;  // 16-byte units (B >= 128)
-    if (n16 * 2 > slot_words) {  // cannot happen: wcap bounds every delta
-      if (lane == 0) atomicOr(err, err_bit(MS_E_CORRUPT));
-    } else {
-      const uint4* src = reinterpret_cast<const uint4*>(packed);
-      uint4* dst = reinterpret_cast<uint4*>(slots + item * slot_words);
-      for (uint32_t m = lane; m < n16; m += 32) dst[m] = src[m];
-    }
-    if (lane == 0) {
-      wk[item] = w;
-      e.ref[item] = row0 + row_offset;
-    }
-    __syncwarp();
   }
 }
 
