@@ -153,10 +153,38 @@ __device__ __forceinline__ uint32_t lane_rows(const uint32_t* __restrict__ p, co
   }
 }
 
+// Words [Q0, Q0 + NW) of a lane's W words (zero past W) with the widest vector
+// shared-memory loads their alignment allows: lanes are W words apart, so scalar
+// loads at an even W hit the same bank gcd(W, 32) ways (8 at W = 40); 16-byte
+// loads leave at most two lanes of a quarter-warp on one bank group.
+template <int W, int Q0, int NW, bool VEC>
+__device__ __forceinline__ void load_lane_range(const uint32_t* __restrict__ p, uint32_t (&r)[NW]) {
+  constexpr int V = !VEC ? 1 : (W % 4 == 0 && Q0 % 4 == 0) ? 4 : ((W % 2 == 0 && Q0 % 2 == 0) ? 2 : 1);
+#pragma unroll
+  for (int i = 0; i < NW; i += V) {
+    if (V == 4 && i + 3 < NW && Q0 + i + 3 < W) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + Q0 + i);
+      r[i] = v.x; r[i + 1] = v.y; r[i + 2] = v.z; r[i + 3] = v.w;
+    } else if (V >= 2 && i + 1 < NW && Q0 + i + 1 < W) {
+      const uint2 v = *reinterpret_cast<const uint2*>(p + Q0 + i);
+      r[i] = v.x; r[i + 1] = v.y;
+      if (V == 4) {
+#pragma unroll
+        for (int k = 2; k < V; ++k)
+          if (i + k < NW) r[i + k] = (Q0 + i + k < W) ? p[Q0 + i + k] : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (i + k < NW) r[i + k] = (Q0 + i + k < W) ? p[Q0 + i + k] : 0u;
+    }
+  }
+}
+
 // W > 32: the same 32 rows in two halves of 16 rows (16*W bits each) so that at
 // most W/2 + 2 words are live in registers; the second half starts at the
 // compile-time bit offset 16*W.
-template <int W, int H>
+template <int W, int H, bool VEC>
 __device__ __forceinline__ uint32_t half_rows(const uint32_t* __restrict__ p, const FastPred& pr, uint64_t ref,
                                               uint64_t d) {
   constexpr int B0 = H * 16 * W;       // first bit of this half
@@ -164,8 +192,7 @@ __device__ __forceinline__ uint32_t half_rows(const uint32_t* __restrict__ p, co
   constexpr int NW = ((B0 & 31) + 16 * W + 31) / 32 + 1;
   constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
   uint32_t r[NW];
-#pragma unroll
-  for (int i = 0; i < NW; ++i) r[i] = (Q0 + i < W) ? p[Q0 + i] : 0u;
+  load_lane_range<W, Q0, NW, VEC>(p, r);
   uint32_t m = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -190,14 +217,13 @@ __device__ __forceinline__ uint32_t half_rows(const uint32_t* __restrict__ p, co
 // low-word test runs for every row (one funnel shift, one add, one compare); the
 // high bits are checked only for the candidates it leaves (at most as many as the
 // matches plus the rare rows whose low word alone falls in the interval).
-template <int W, int H>
+template <int W, int H, bool VEC>
 __device__ __forceinline__ uint32_t half_low32(const uint32_t* __restrict__ p, uint32_t a, uint32_t s) {
   constexpr int B0 = H * 16 * W;
   constexpr int Q0 = B0 >> 5;
   constexpr int NW = ((B0 & 31) + 16 * W + 31) / 32 + 1;
   uint32_t r[NW];
-#pragma unroll
-  for (int i = 0; i < NW; ++i) r[i] = (Q0 + i < W) ? p[Q0 + i] : 0u;
+  load_lane_range<W, Q0, NW, VEC>(p, r);
   uint32_t m = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -208,12 +234,12 @@ __device__ __forceinline__ uint32_t half_low32(const uint32_t* __restrict__ p, u
   return m;
 }
 
-template <int W>
+template <int W, bool VEC>
 __device__ __forceinline__ uint32_t lane_rows_wide(const uint32_t* __restrict__ p, const FastPred& pr,
                                                    uint64_t ref) {
   const uint64_t d = pr.lo - ref;
   if (!pr.is_bitmap && d + pr.span >= d && d + pr.span <= 0xffffffffull) {
-    uint32_t cand = half_low32<W, 0>(p, (uint32_t)d, (uint32_t)pr.span) | half_low32<W, 1>(p, (uint32_t)d,
+    uint32_t cand = half_low32<W, 0, VEC>(p, (uint32_t)d, (uint32_t)pr.span) | half_low32<W, 1, VEC>(p, (uint32_t)d,
                                                                                            (uint32_t)pr.span);
     uint32_t m = cand;
     while (cand) {  // confirm: the high W - 32 bits of the candidate's code are zero
@@ -226,14 +252,19 @@ __device__ __forceinline__ uint32_t lane_rows_wide(const uint32_t* __restrict__ 
     }
     return pr.neg ? ~m : m;
   }
-  return half_rows<W, 0>(p, pr, ref, d) | half_rows<W, 1>(p, pr, ref, d);
+  return half_rows<W, 0, VEC>(p, pr, ref, d) | half_rows<W, 1, VEC>(p, pr, ref, d);
 }
 
+// VEC: the wide cores stage their words with vector loads (the per-warp-ring core,
+// launched for widths > 32); the streamed core (widths <= 32, a wider block only
+// under an understated max_width hint) keeps scalar loads, which keep it free of
+// spills.
+template <bool VEC>
 __device__ __forceinline__ uint32_t lane_dispatch(uint32_t w, const uint32_t* p, const FastPred& pr, uint64_t ref) {
   switch (w) {
 #define MS_LANE_CASE(W) \
   case W:               \
-    return W <= 32 ? lane_rows<(W <= 32 ? W : 1)>(p, pr, ref) : lane_rows_wide<(W > 32 ? W : 33)>(p, pr, ref);
+    return W <= 32 ? lane_rows<(W <= 32 ? W : 1)>(p, pr, ref) : lane_rows_wide<(W > 32 ? W : 33), VEC>(p, pr, ref);
     MS_LANE_CASE(0) MS_LANE_CASE(1) MS_LANE_CASE(2) MS_LANE_CASE(3) MS_LANE_CASE(4) MS_LANE_CASE(5)
     MS_LANE_CASE(6) MS_LANE_CASE(7) MS_LANE_CASE(8) MS_LANE_CASE(9) MS_LANE_CASE(10) MS_LANE_CASE(11)
     MS_LANE_CASE(12) MS_LANE_CASE(13) MS_LANE_CASE(14) MS_LANE_CASE(15) MS_LANE_CASE(16) MS_LANE_CASE(17)
@@ -252,7 +283,27 @@ __device__ __forceinline__ uint32_t lane_dispatch(uint32_t w, const uint32_t* p,
 }
 
 // ---- sum core: the same lane-consecutive unpack, accumulating the codes
-template <int W>
+// W > 32: rows [16H, 16H + 16) of the lane, words staged in registers by vector loads
+template <int W, int H, bool VEC>
+__device__ __forceinline__ uint64_t lane_sum_half(const uint32_t* __restrict__ p) {
+  constexpr int B0 = H * 16 * W;
+  constexpr int Q0 = B0 >> 5;
+  constexpr int NW = ((B0 & 31) + 16 * W + 31) / 32 + 1;
+  constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
+  uint32_t r[NW];
+  load_lane_range<W, Q0, NW, VEC>(p, r);
+  uint64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int bit = (B0 & 31) + i * W, q = bit >> 5, sh = bit & 31;
+    const uint32_t lo = __funnelshift_r(r[q], r[q + 1], sh);
+    const uint32_t hi = __funnelshift_r(r[q + 1], r[q + 2 < NW ? q + 2 : NW - 1], sh);
+    acc += (((uint64_t)hi << 32) | lo) & mask;
+  }
+  return acc;
+}
+
+template <int W, bool VEC>
 __device__ __forceinline__ uint64_t lane_sum(const uint32_t* __restrict__ p) {
   if constexpr (W == 0) {
     return 0;
@@ -264,28 +315,16 @@ __device__ __forceinline__ uint64_t lane_sum(const uint32_t* __restrict__ p) {
     for (int i = 0; i < 32; ++i) acc += code_at<W>(r, i);
     return acc;
   } else {
-    uint64_t acc = 0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int B0 = h * 16 * W, Q0 = B0 >> 5;
-      constexpr uint64_t mask = W >= 64 ? ~0ull : ((1ull << (W & 63)) - 1);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int bit = (B0 & 31) + i * W, q = Q0 + (bit >> 5), sh = bit & 31;
-        const uint32_t w0 = p[q], w1 = q + 1 < W ? p[q + 1] : 0u, w2 = q + 2 < W ? p[q + 2] : 0u;
-        const uint64_t code = (((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh)) & mask;
-        acc += code;
-      }
-    }
-    return acc;
+    return lane_sum_half<W, 0, VEC>(p) + lane_sum_half<W, 1, VEC>(p);
   }
 }
 
+template <bool VEC>
 __device__ __forceinline__ uint64_t lane_sum_dispatch(uint32_t w, const uint32_t* p) {
   switch (w) {
 #define MS_SUM_CASE(W) \
   case W:              \
-    return lane_sum<W>(p);
+    return lane_sum<W, VEC>(p);
     MS_SUM_CASE(0) MS_SUM_CASE(1) MS_SUM_CASE(2) MS_SUM_CASE(3) MS_SUM_CASE(4) MS_SUM_CASE(5) MS_SUM_CASE(6)
     MS_SUM_CASE(7) MS_SUM_CASE(8) MS_SUM_CASE(9) MS_SUM_CASE(10) MS_SUM_CASE(11) MS_SUM_CASE(12)
     MS_SUM_CASE(13) MS_SUM_CASE(14) MS_SUM_CASE(15) MS_SUM_CASE(16) MS_SUM_CASE(17) MS_SUM_CASE(18)
@@ -302,6 +341,7 @@ __device__ __forceinline__ uint64_t lane_sum_dispatch(uint32_t w, const uint32_t
       return 0;
   }
 }
+
 
 enum : int { CORE_SELECT = 0, CORE_SUM = 1 };
 
@@ -414,9 +454,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, kMinBlocks) select_fast_kerne
       const uint32_t* p = buf + stage * kPairBufU32 + (half ? 16 * wa : 0) + hl * w;
       if (valid) {
         if constexpr (CORE == CORE_SUM) {
-          sum_acc += lane_sum_dispatch(w, p) + (hl == 0 ? (uint64_t)kSegRows * ref : 0ull);
+          sum_acc += lane_sum_dispatch<true>(w, p) + (hl == 0 ? (uint64_t)kSegRows * ref : 0ull);
         } else {
-          m = lane_dispatch(w, p, pred, ref);
+          m = lane_dispatch<true>(w, p, pred, ref);
         }
       }
     }

@@ -217,9 +217,9 @@ __global__ void __launch_bounds__((1 + 2 * kSsMaxStages) * 32, 1)
         } else {
           const uint32_t* pp = base + 2 * word + hl * w;
           if constexpr (CORE == CORE_SUM) {
-            sum_acc += lane_sum_dispatch(w, pp) + (hl == 0 ? (uint64_t)kSegRows * ref : 0ull);
+            sum_acc += lane_sum_dispatch<false>(w, pp) + (hl == 0 ? (uint64_t)kSegRows * ref : 0ull);
           } else {
-            mword = lane_dispatch(w, pp, pred, ref);
+            mword = lane_dispatch<false>(w, pp, pred, ref);
           }
         }
       }
