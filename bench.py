@@ -358,15 +358,24 @@ def run_ours(args):
             ent["achieved_gbs"] = alg[k] / (avg * 1e-3) / 1e9
             ent["frac_of_peak"] = ent["achieved_gbs"] / peak
         kernels[k] = ent
+    # ALU roofline of the issue-bound encoder: executed warp instructions per launch
+    # (ncu, this build, this workload) over its event-timed duration, against the
+    # issue peak (4 schedulers x SMs x the SM clock sampled during the run)
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    tj = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    clk_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    issue_peak = 4 * props.multi_processor_count * clk_mhz * 1e6
+    for k, ins in tj.get("_inst", {}).items():
+        if k in kernels and args.n_log2 == 32 and world == 1:
+            a = ins / (kernels[k]["avg_ms"] * 1e-3)
+            kernels[k]["alu"] = {"warp_inst_per_launch": ins, "achieved_ginst_s": a / 1e9,
+                                 "issue_peak_ginst_s": issue_peak / 1e9, "frac": a / issue_peak}
     dom_name = max(prof.items(), key=lambda kv: kv[1][1])[0]
     dom = kernels[dom_name]
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        if args.n_log2 == 32 and world == 1:  # captured at this workload (one GPU, 2^32 rows)
-            traffic = tj.get(dom_name)
-            traffic_src = tj.get("_about")
+    if tj and args.n_log2 == 32 and world == 1:  # captured at this workload (one GPU, 2^32 rows)
+        traffic = tj.get(dom_name)
+        traffic_src = tj.get("_about")
     step_ms = ms_total / args.steps
     chain_alg = x_bytes + bytes_pos + gather_bytes + 2 * bytes_yp
     value = n * args.steps / (ms_total * 1e-3) / 1e9

@@ -1,0 +1,48 @@
+#!/usr/bin/env python3
+"""profiles/ncu_traffic.json from an `ncu --set full` raw export of the bench's
+hot kernels: per launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)
+and executed warp instructions (smsp__inst_executed.sum), keyed by the bench's
+profiling names. usage: python tools/ncu_traffic.py RAW_CSV ABOUT > profiles/ncu_traffic.json"""
+import csv
+import json
+import sys
+
+NAMES = [("select_stream", "select_stream"), ("project_stream", "project_stream"), ("pos_slot", "pos_slot"),
+         ("pos_copy", "pos_copy"), ("project_copy", "project_copy"), ("sum_stream", "sum_stream")]
+
+
+def scale(v, unit):
+    f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+    return float(v.replace(",", "")) * f
+
+
+def main():
+    rows = [r for r in csv.reader(open(sys.argv[1])) if r]
+    hdr, units = rows[0], rows[1]
+    ix = {h: i for i, h in enumerate(hdr)}
+    acc = {}
+    for r in rows[2:]:
+        name = r[ix["Kernel Name"]]
+        key = next((k for s, k in NAMES if s in name), None)
+        if key is None:
+            continue
+        rd = scale(r[ix["dram__bytes_read.sum"]], units[ix["dram__bytes_read.sum"]])
+        wr = scale(r[ix["dram__bytes_write.sum"]], units[ix["dram__bytes_write.sum"]])
+        ins = float(r[ix["smsp__inst_executed.sum"]].replace(",", ""))
+        a = acc.setdefault(key, [0.0, 0.0, 0])
+        a[0] += rd + wr
+        a[1] += ins
+        a[2] += 1
+    # pos_slot: the dense launch and the deferred-blocks launch form one encoder step
+    out = {"_about": sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]}
+    inst = {}
+    for k, (b, ins, c) in acc.items():
+        per = 2 if k == "pos_slot" and c % 2 == 0 else 1
+        out[k] = int(b / c * per)
+        inst[k] = int(ins / c * per)
+    out["_inst"] = inst
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
