@@ -542,6 +542,7 @@ ms_status positions_from_mask(const Ctx& ctx, uint32_t* bits, uint32_t* seg_info
   const bool wscan = pos_delta || pos_slots;
   const uint64_t o_wk = wscan ? sc.add(4 * (items_max + 1), false) : 0;
   const uint64_t o_cwx = wscan ? sc.add(8 * (items_max + 2), false) : 0;
+  const uint64_t o_dlc = pos_delta ? sc.add(4 * (items_max + 2), true) : 0;  // deferred blocks: count, entries
   const uint64_t o_st3 = wscan ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
   const uint64_t o_tk3 = wscan ? sc.add(8, true) : 0;
   if (!sc.commit()) return MS_E_NOMEM;
@@ -632,7 +633,7 @@ ms_status positions_from_mask(const Ctx& ctx, uint32_t* bits, uint32_t* seg_info
         pos_delta && f.format == MS_DELTA_BP
             ? launch_positions_delta(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset,
                                      sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
-                                     sc.at<uint32_t>(o_tk3), slots, slot_words, err, ctx.s)
+                                     sc.at<uint32_t>(o_tk3), slots, slot_words, sc.at<uint32_t>(o_dlc), err, ctx.s)
         : pos_slots
             ? launch_positions_slots(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset, slots,
                                      slot_words, sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx),

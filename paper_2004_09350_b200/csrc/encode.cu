@@ -58,8 +58,8 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
 
 cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                                    uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
-                                   uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* err,
-                                   cudaStream_t s) {
+                                   uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* dlist,
+                                   uint32_t* err, cudaStream_t s) {
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   const uint64_t n_full = e.n_out / e.G;
   if (!n_items) return cudaSuccess;
@@ -75,22 +75,22 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
   };
   if (slots && n_full) {  // single walk: slots, scan, copy
     const size_t smem = (size_t)kPdWarps * kPdWarpU32 * 4;
-    // dense: a mean mask span per block under 384 words (most blocks take pd_item512);
-    // the blocks it defers are walked by a second launch
-    const bool dense = e.G == 512 && n_words < 384 * n_full;
+    // B = 512: blocks whose span fits take pd_item512, the others (sparse regions, the
+    // block before the last) are deferred to a second launch that walks them
+    const bool dense = e.G == 512;
     {
       ProfScope prof_("pos_slot", s);
       if (dense) {
         const int grid = grid_for(pos_slot_kernel<kPdDense>, smem, n_items);
         pos_slot_kernel<kPdDense><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items,
-                                                                   slots, slot_words, wk, err);
+                                                                   slots, slot_words, wk, dlist, err);
         pos_slot_kernel<kPdDeferredOnly><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e,
-                                                                          n_items, slots, slot_words, wk, err);
+                                                                          n_items, slots, slot_words, wk, dlist, err);
         count_launch();
       } else {
         const int grid = grid_for(pos_slot_kernel<kPdAll>, smem, n_items);
         pos_slot_kernel<kPdAll><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items,
-                                                                 slots, slot_words, wk, err);
+                                                                 slots, slot_words, wk, dlist, err);
       }
     }
     cudaError_t r = cudaGetLastError();

@@ -439,12 +439,11 @@ __device__ __forceinline__ void pd_store_slot(uint64_t item, uint32_t w, uint64_
   __syncwarp();
 }
 
-// MODE kPdDense (B = 512, mean span < 384 words): pd_item512 only; a block whose
-// span does not fit (and the block before the last) is marked kPdDeferred in wk
-// and left to a kPdDeferredOnly launch, which walks only the marked blocks. The
-// walk's registers stay out of the fast path. kPdAll: the walk for every block.
+// MODE kPdDense (B = 512): pd_item512 only; a block whose span does not fit (and
+// the block before the last) is appended to dlist (dlist[0]: count) and left to a
+// kPdDeferredOnly launch, whose warps take the listed blocks one each. The walk's
+// registers stay out of the fast path. kPdAll: the walk for every block.
 constexpr int kPdAll = 0, kPdDense = 1, kPdDeferredOnly = 2;
-constexpr uint32_t kPdDeferred = 0xffffffffu;
 
 // One full block by the walk (pd_item_walk; two walks past 2^32 rows) into its slot.
 __device__ __forceinline__ void pd_walk_block(const uint32_t* __restrict__ bits, uint64_t n_words, uint64_t row0,
@@ -473,7 +472,8 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
                                                                  const uint64_t* __restrict__ gstart,
                                                                  uint64_t row_offset, PosEnc e, uint64_t n_items,
                                                                  uint64_t* __restrict__ slots, uint32_t slot_words,
-                                                                 uint32_t* __restrict__ wk, uint32_t* err) {
+                                                                 uint32_t* __restrict__ wk, uint32_t* dlist,
+                                                                 uint32_t* err) {
   extern __shared__ __align__(16) uint32_t pd_sm[];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* stage = pd_sm + (size_t)wid * kPdWarpU32;
@@ -481,16 +481,12 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
   const uint64_t n_full = e.n_out / B;
   const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
   const uint64_t gw = (uint64_t)blockIdx.x * kPdWarps + wid;
-  if (MODE == kPdDeferredOnly) {  // the marked blocks: 32 wk words per warp step, a ballot
-    for (uint64_t b0 = gw * 32; b0 < n_full; b0 += nwarps * 32) {
-      const uint64_t it = b0 + lane;
-      uint32_t m = __ballot_sync(kFull, it < n_full && __ldg(wk + it) == kPdDeferred);
-      while (m) {
-        const uint64_t item = b0 + (__ffs(m) - 1);
-        m &= m - 1;
-        pd_walk_block(bits, n_words, __ldg(gstart + item) - row_offset, item, row_offset, e, slots, slot_words, wk,
-                      stage, lane, err);
-      }
+  if (MODE == kPdDeferredOnly) {  // the listed blocks, one per warp
+    const uint32_t nd = *reinterpret_cast<volatile uint32_t*>(dlist);
+    for (uint64_t i = gw; i < nd; i += nwarps) {
+      const uint64_t item = __ldg(dlist + 1 + i);
+      pd_walk_block(bits, n_words, __ldg(gstart + item) - row_offset, item, row_offset, e, slots, slot_words, wk,
+                    stage, lane, err);
     }
     return;
   }
@@ -513,9 +509,8 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
       if (item + 1 < n_items && (rowE >> 5) - (row0 >> 5) < 512) {
         const uint32_t w = pd_item512(bits, row0, rowE, reinterpret_cast<uint16_t*>(stage), lane, err);
         pd_store_slot(item, w, row0 + row_offset, e, slots, slot_words, wk, stage, lane, err);
-      } else {
-        if (lane == 0) wk[item] = kPdDeferred;
-        __syncwarp();
+      } else if (lane == 0) {
+        dlist[1 + atomicAdd(dlist, 1u)] = (uint32_t)item;
       }
     } else {
       pd_walk_block(bits, n_words, row0, item, row_offset, e, slots, slot_words, wk, stage, lane, err);
