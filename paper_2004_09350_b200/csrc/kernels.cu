@@ -389,47 +389,64 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(uint64_t* v, uint64_t 
   }
 }
 
+// Warp-striped apply: warp w of the CTA owns the tile's elements [256w, 256w + 256),
+// lane l the elements 256w + 32q + l (q < 8): every load and every epilogue store
+// of the warp is one contiguous run (the thread-consecutive mapping touched 32
+// lines per instruction). Offsets: a warp scan per row q with the rows' carry,
+// then the warps' totals across the CTA.
 template <class In, class Epi>
 __global__ void __launch_bounds__(kThreads) scan_apply_kernel(In in, Epi epi, uint64_t N, const uint64_t* tile_off) {
-  __shared__ uint64_t scan_sm[16];
+  __shared__ uint64_t wsum[kThreads / 32 + 1];
   const uint64_t n_items = (N + kChunk - 1) / kChunk;
-  const int tid = threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t key = 0;  // the largest key this thread saw: one atomic per CTA at the end
   // the thread's values one tile ahead: the tile's load round trip overlaps the
   // previous tile's scan and epilogue
   uint64_t nxt[kVPT];
   {
-    const uint64_t b0 = (uint64_t)blockIdx.x * kChunk + tid * kVPT;
+    const uint64_t b0 = (uint64_t)blockIdx.x * kChunk + wid * (32 * kVPT) + lane;
 #pragma unroll
-    for (int q = 0; q < kVPT; ++q) nxt[q] = b0 + q < N ? in(b0 + q) : 0;
+    for (int q = 0; q < kVPT; ++q) nxt[q] = b0 + 32 * q < N ? in(b0 + 32 * q) : 0;
   }
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const uint64_t base = item * kChunk + tid * kVPT;
+    const uint64_t base = item * kChunk + wid * (32 * kVPT) + lane;
     uint64_t v[kVPT];
-    uint64_t tsum = 0;
 #pragma unroll
-    for (int q = 0; q < kVPT; ++q) {
-      v[q] = nxt[q];
-      tsum += v[q];
-    }
+    for (int q = 0; q < kVPT; ++q) v[q] = nxt[q];
     const uint64_t toff = tile_off[item];
     {
       const uint64_t b1 = base + (uint64_t)gridDim.x * kChunk;
 #pragma unroll
-      for (int q = 0; q < kVPT; ++q) nxt[q] = b1 + q < N ? in(b1 + q) : 0;
+      for (int q = 0; q < kVPT; ++q) nxt[q] = b1 + 32 * q < N ? in(b1 + 32 * q) : 0;
     }
-    const uint64_t ex = cta_excl_scan(tsum, scan_sm, nullptr);  // ends with a barrier
-    uint64_t off = toff + ex;
+    uint64_t ex[kVPT];
+    uint64_t carry = 0;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
-      if (base + q < N) {
-        epi(base + q, off, v[q]);
-        const uint64_t kq = epi.key(base + q);
-        key = kq > key ? kq : key;
-        if (base + q == N - 1) epi.total(off + v[q]);
-      }
-      off += v[q];
+      const uint64_t inc = warp_incl_scan(v[q]);
+      ex[q] = carry + inc - v[q];
+      carry += __shfl_sync(kFull, inc, 31);
     }
+    if (lane == 0) wsum[wid] = carry;
+    __syncthreads();
+    if (wid == 0) {
+      const uint64_t x = lane < kThreads / 32 ? wsum[lane] : 0;
+      const uint64_t xi = warp_incl_scan(x);
+      if (lane < kThreads / 32) wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    const uint64_t wb = toff + wsum[wid];
+#pragma unroll
+    for (int q = 0; q < kVPT; ++q) {
+      const uint64_t idx = base + 32 * q;
+      if (idx < N) {
+        epi(idx, wb + ex[q], v[q]);
+        const uint64_t kq = epi.key(idx);
+        key = kq > key ? kq : key;
+        if (idx == N - 1) epi.total(wb + ex[q] + v[q]);
+      }
+    }
+    __syncthreads();  // wsum is rewritten by the next tile
   }
   cta_max_key(epi, key);
 }
