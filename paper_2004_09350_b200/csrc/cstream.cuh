@@ -13,8 +13,10 @@
 //   widths  lane b: w_b (DYN: ebw(max), FOR: ebw(max - min), DELTA: ebw(max d)),
 //           exclusive prefix over the tile's blocks -> bw, ref, slot offsets;
 //   pack    thread t of the pair builds u32 words t, t + 64, ... of each block
-//           from the <= 3 codes that overlap it and stores them to the tile's
-//           slot (coalesced); rows past the last full block go to the remainder.
+//           from the codes that overlap it, at the block's width as a
+//           compile-time constant (switch over 1..64), and stores them to the
+//           tile's slot (coalesced); rows past the last full block go to the
+//           remainder.
 // The scan of bw and tile_copy_kernel then place the tiles as for the engine.
 #pragma once
 #include "common.cuh"
@@ -37,6 +39,58 @@ __host__ __device__ constexpr size_t cs_smem_bytes() {
 }
 
 __device__ __forceinline__ void cs_bar(uint32_t id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id + 1) : "memory"); }
+
+// u32 words m = tt, tt + 64, ... of a block of B codes at the compile-time width W
+// (B * W / 32 words): word m starts inside code j = 32m / W (a division by a
+// constant) at bit sh = 32m - jW; the codes j + 1, ... that fill it follow, at
+// most 32 / W + 1 of them (DELTA: code = v_j - v_{j-1}, code 0 = 0; else v - sub).
+template <int W, bool DELTA>
+__device__ __forceinline__ void cs_pack_block(const uint64_t* __restrict__ cb, uint64_t sub, uint32_t B,
+                                              uint32_t* __restrict__ dst, uint32_t tt) {
+  constexpr int K = 32 / W + 1;  // codes after the first that may overlap one word
+  const uint32_t nw = (uint32_t)W * (B >> 5);
+  for (uint32_t m = tt; m < nw; m += 32 * kCsPair) {
+    const uint32_t bit0 = m * 32, j = bit0 / (uint32_t)W, sh = bit0 - j * (uint32_t)W;
+    uint64_t v = cb[j];
+    uint64_t prev = DELTA ? (j ? cb[j - 1] : v) : sub;  // DELTA: the previous value carried along
+    uint64_t acc = (v - prev) >> sh;
+    uint32_t filled = (uint32_t)W - sh;
+#pragma unroll
+    for (int k = 1; k <= K; ++k) {
+      if (filled < 32) {
+        if (DELTA) prev = v;
+        v = cb[j + k];
+        acc |= (v - prev) << filled;
+        filled += W;
+      }
+    }
+    dst[m] = (uint32_t)acc;
+  }
+}
+
+template <bool DELTA>
+__device__ __forceinline__ void cs_pack_dispatch(uint32_t w, const uint64_t* cb, uint64_t sub, uint32_t B,
+                                                 uint32_t* dst, uint32_t tt) {
+  switch (w) {
+#define MS_CS_CASE(W) \
+  case W:             \
+    cs_pack_block<W, DELTA>(cb, sub, B, dst, tt); \
+    break;
+    MS_CS_CASE(1) MS_CS_CASE(2) MS_CS_CASE(3) MS_CS_CASE(4) MS_CS_CASE(5) MS_CS_CASE(6) MS_CS_CASE(7)
+    MS_CS_CASE(8) MS_CS_CASE(9) MS_CS_CASE(10) MS_CS_CASE(11) MS_CS_CASE(12) MS_CS_CASE(13) MS_CS_CASE(14)
+    MS_CS_CASE(15) MS_CS_CASE(16) MS_CS_CASE(17) MS_CS_CASE(18) MS_CS_CASE(19) MS_CS_CASE(20) MS_CS_CASE(21)
+    MS_CS_CASE(22) MS_CS_CASE(23) MS_CS_CASE(24) MS_CS_CASE(25) MS_CS_CASE(26) MS_CS_CASE(27) MS_CS_CASE(28)
+    MS_CS_CASE(29) MS_CS_CASE(30) MS_CS_CASE(31) MS_CS_CASE(32) MS_CS_CASE(33) MS_CS_CASE(34) MS_CS_CASE(35)
+    MS_CS_CASE(36) MS_CS_CASE(37) MS_CS_CASE(38) MS_CS_CASE(39) MS_CS_CASE(40) MS_CS_CASE(41) MS_CS_CASE(42)
+    MS_CS_CASE(43) MS_CS_CASE(44) MS_CS_CASE(45) MS_CS_CASE(46) MS_CS_CASE(47) MS_CS_CASE(48) MS_CS_CASE(49)
+    MS_CS_CASE(50) MS_CS_CASE(51) MS_CS_CASE(52) MS_CS_CASE(53) MS_CS_CASE(54) MS_CS_CASE(55) MS_CS_CASE(56)
+    MS_CS_CASE(57) MS_CS_CASE(58) MS_CS_CASE(59) MS_CS_CASE(60) MS_CS_CASE(61) MS_CS_CASE(62) MS_CS_CASE(63)
+    MS_CS_CASE(64)
+#undef MS_CS_CASE
+    default:
+      break;
+  }
+}
 
 __global__ void __launch_bounds__(kCsThreads, 1)
     compress_stream_kernel(const uint64_t* __restrict__ in, uint64_t n, OutView o, uint32_t* err) {
@@ -144,32 +198,17 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       }
     }
     cs_bar(p);
-    // pack: thread tt builds u32 words tt, tt + 64, ... of each block from the codes overlapping them
+    // pack: thread tt builds u32 words tt, tt + 64, ... of each block from the codes overlapping them,
+    // at the block's width as a compile-time constant (cs_pack_block<W>)
     uint32_t* slot32 = reinterpret_cast<uint32_t*>(o.slots + t * kChunk);
     for (uint32_t b = 0; b < nbc; ++b) {
       const uint32_t wb = W.w[b];
       if (!wb) continue;
       const uint64_t* cb = V + (b << lg);
       const uint64_t sub = is_for ? W.lo[b] : 0ull;
-      const uint32_t nw = wb << (lg - 5);  // B * w / 32 words
-      const uint32_t magic = 0xffffffffu / wb + 1u;
       uint32_t* dst = slot32 + (W.ex[b] << (lg - 5));
-      for (uint32_t m = tt; m < nw; m += 32 * kCsPair) {
-        const uint32_t bit0 = m * 32;
-        uint32_t j = div_small(bit0, wb, magic);
-        // codes j, j+1, ... (DELTA: differences, the previous value carried along)
-        uint64_t v = cb[j];
-        uint64_t prev = is_delta ? (j ? cb[j - 1] : v) : sub;
-        uint64_t acc = (v - prev) >> (bit0 - j * wb);
-        for (++j; j < B; ++j) {
-          const uint32_t jb = j * wb;
-          if (jb >= bit0 + 32) break;
-          if (is_delta) prev = v;
-          v = cb[j];
-          acc |= (v - prev) << (jb - bit0);
-        }
-        dst[m] = (uint32_t)acc;
-      }
+      if (is_delta) cs_pack_dispatch<true>(wb, cb, sub, B, dst, tt);
+      else cs_pack_dispatch<false>(wb, cb, sub, B, dst, tt);
     }
     // rows past the last full block: the uncompressed remainder
     for (uint32_t i = nmain + tt; i < cnt; i += 32 * kCsPair) o.rem[r0 + i - nbm] = V[i];
