@@ -7,8 +7,10 @@ import csv
 import json
 import sys
 
-NAMES = [("select_stream", "select_stream"), ("project_stream", "project_stream"), ("pos_slot", "pos_slot"),
-         ("pos_copy", "pos_copy"), ("project_copy", "project_copy"), ("sum_stream", "sum_stream")]
+# kernel name -> the bench's profiling scope (first match wins)
+NAMES = [("select_stream_kernel<2, 1>", "sum_stream"), ("select_stream_kernel<", "select_stream"),
+         ("project_stream_kernel", "project_stream"), ("pos_copy_kernel<32>", "project_copy"),
+         ("pos_copy_kernel<8>", "pos_copy"), ("pos_slot_kernel<2>", "pos_slot+"), ("pos_slot_kernel", "pos_slot")]
 
 
 def scale(v, unit):
@@ -33,13 +35,15 @@ def main():
         a[0] += rd + wr
         a[1] += ins
         a[2] += 1
-    # pos_slot: the dense launch and the deferred-blocks launch form one encoder step
+    # pos_slot: the dense launch plus the deferred-blocks launch form one encoder step
+    extra = acc.pop("pos_slot+", None)
     out = {"_about": sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]}
     inst = {}
     for k, (b, ins, c) in acc.items():
-        per = 2 if k == "pos_slot" and c % 2 == 0 else 1
-        out[k] = int(b / c * per)
-        inst[k] = int(ins / c * per)
+        if k == "pos_slot" and extra:
+            b, ins = b + extra[0], ins + extra[1]
+        out[k] = int(b / c)
+        inst[k] = int(ins / c)
     out["_inst"] = inst
     print(json.dumps(out, indent=1))
 
