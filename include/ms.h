@@ -254,7 +254,10 @@ MS_API ms_status ms_join(const ms_ctx *ctx, const ms_column *left, const ms_colu
  * for k < bitmap_bits), in out_fmt. Equal to project(positions, select(project(
  * keys, positions), IN_BITMAP)) — the fused form (K7) gathers the keys of each
  * 512-position block into shared memory and tests them there, so the projected
- * keys are never written. MS_E_RANGE if a position lies outside the keys. */
+ * keys are never written; the surviving positions are set in a mask over the keys'
+ * rows and encoded by the select output layer. MS_E_RANGE if a position lies
+ * outside the keys; MS_E_INVALID if the positions are not strictly increasing (as
+ * every positions column this library produces is). */
 MS_API ms_status ms_semijoin(const ms_ctx *ctx, const ms_column *keys, const ms_column *positions,
                              uint64_t row_offset, const uint64_t *bitmap, uint64_t bitmap_bits, ms_fmt out_fmt,
                              ms_column *out);

@@ -1468,22 +1468,22 @@ ms_status ms_semijoin(const ms_ctx* ctx_, const ms_column* keys, const ms_column
     release(ctx, &idx);
     return st;
   }
-  const uint64_t NS = (n1 + kSegRows - 1) / kSegRows;
+  // fused (K7, row space): the surviving positions as a mask over the keys' rows,
+  // turned into pos2 by the select output layer
+  (void)n1;
+  const uint64_t nk = keys->n;
+  const uint64_t NS = (nk + kSegRows - 1) / kSegRows;
   Scratch sc(ctx);
   const uint64_t o_meta = sc.add(64, true);
-  const uint64_t o_bits = sc.add(4 * NS * kSegWords, false);
+  const uint64_t o_bits = sc.add(4 * NS * kSegWords, true);
   const uint64_t o_seg = sc.add(4 * (NS + 1), false);
   if (!sc.commit()) return MS_E_NOMEM;
   uint32_t* err = sc.at<uint32_t>(o_meta);
-  MS_TRY_CUDA(launch_semi_mask(view_of(positions), view_of(keys), row_offset, bitmap, bitmap_bits,
-                               sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), err, ctx.s));
-  // the surviving ranks of pos1 (DELTA_BP{512}, the select output layer), then pos1 at those ranks
-  ms_column idx;
-  MS_TRY(positions_from_mask(ctx, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, n1, 0,
-                             ms_fmt{MS_DELTA_BP, 0, 512, 0}, err, &idx));
-  const ms_status st = ms_project(ctx_, positions, &idx, 0, out_fmt, out);
-  release(ctx, &idx);
-  return st;
+  MS_TRY_CUDA(launch_semi_rows(view_of(positions), view_of(keys), row_offset, bitmap, bitmap_bits,
+                               sc.at<uint32_t>(o_bits), err, ctx.s));
+  if (NS) MS_TRY_CUDA(launch_seg_info(sc.at<uint32_t>(o_bits), NS, sc.at<uint32_t>(o_seg), ctx.s));
+  return positions_from_mask(ctx, sc.at<uint32_t>(o_bits), sc.at<uint32_t>(o_seg), NS, nk, row_offset, out_fmt, err,
+                             out);
 }
 
 ms_status ms_check_errors(const ms_ctx* ctx_) {

@@ -119,14 +119,28 @@ cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_
 // pos2 = {p in pos1 : bitmap[keys[p - row_offset]]} (the star-schema semi-join of
 // BJ.c4, D-16). One warp per 512-position block of pos1: decode the block,
 // gather the keys at its positions (ProjectSource: header broadcast, bulk L2
-// prefetch, 4 gathers in flight per lane), test the bitmap, and write one 32-bit
-// mask word per 32 ranks of pos1 plus the block's count | last << 16 — the select
-// mask layout over pos1's ranks, so the positions encoders turn it into the
-// surviving ranks. The gathered keys never reach HBM (no k1' column, no select
-// pass over it).
-__global__ void __launch_bounds__(128) semi_mask_kernel(ProjectSource<4> src, uint64_t n1, const uint64_t* bitmap,
-                                                        uint64_t bits_n, uint32_t* __restrict__ bits,
-                                                        uint32_t* __restrict__ seg_info, uint32_t* err) {
+// prefetch, 4 gathers in flight per lane), test the bitmap. The gathered keys
+// never reach HBM (no k1' column, no select pass over it).
+// The row-space form (used by ms_semijoin): the same per-block gather and bitmap
+// test, but a surviving position p sets bit p - row_offset of a mask over the
+// keys' rows (seg_info_kernel then counts its segments), so the select output
+// layer turns the mask straight into pos2 — no positions-through-
+// positions project (which decoded every pos1 block again). Requires pos1
+// strictly increasing (every positions column the library produces); a block
+// that is not, or whose successor does not start after it, flags MS_E_INVALID.
+struct SemiRowSet {
+  const uint64_t* bitmap;
+  uint64_t bits_n, row_offset, n_rows;
+  uint32_t* mask;  // zeroed, 1 bit per row of the keys
+  __device__ __forceinline__ void operator()(uint32_t, uint64_t p, uint64_t v) const {
+    const uint64_t r = p - row_offset;
+    if (p < row_offset || r >= n_rows) return;  // MS_E_RANGE raised by the loader
+    if (v < bits_n && ((__ldg(bitmap + (v >> 6)) >> (v & 63)) & 1ull)) atomicOr(mask + (r >> 5), 1u << (r & 31));
+  }
+};
+
+__global__ void __launch_bounds__(128) semi_rows_kernel(ProjectSource<4> src, uint64_t n1, SemiRowSet set,
+                                                        uint32_t* err) {
   constexpr uint32_t G = kSegRows;
   extern __shared__ __align__(16) uint64_t sj_sm[];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -136,44 +150,42 @@ __global__ void __launch_bounds__(128) semi_mask_kernel(ProjectSource<4> src, ui
   for (uint64_t item = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid; item < n_items; item += NW) {
     const uint64_t r0 = item * G;
     const uint32_t cnt = (uint32_t)min((uint64_t)G, n1 - r0);
-    src.load((uint32_t)item, r0, cnt, P, lane, err);
-    uint32_t c = 0, last = 0;
-#pragma unroll
-    for (int k = 0; k < kSegWords; ++k) {
-      const uint32_t i = k * 32 + lane;
-      bool keep = false;
-      if (i < cnt) {
-        const uint64_t v = P[pidx(i)];
-        keep = v < bits_n && ((__ldg(bitmap + (v >> 6)) >> (v & 63)) & 1ull);
-      }
-      const uint32_t word = __ballot_sync(kFull, keep);
-      if (lane == k) bits[item * kSegWords + k] = word;
-      c += __popc(word);
-      if (word) last = k * 32 + 32 - __clz(word);
+    src.load_with((uint32_t)item, r0, cnt, P, lane, err, set);
+    // strictly increasing inside the block and into the next block
+    bool bad = false;
+    for (uint32_t i = lane + 1; i < cnt; i += 32) bad |= P[pidx(i)] <= P[pidx(i - 1)];
+    if (lane == 0 && r0 + cnt < n1) {  // the next block's first position (DELTA_BP: its base, O(1))
+      const ColView& pc = src.pos;
+      const uint64_t nxt = pc.format == MS_DELTA_BP && ((r0 + cnt) >> pc.log2B) < pc.nb &&
+                                   !((r0 + cnt) & (pc.B - 1))
+                               ? __ldg(pc.ref + ((r0 + cnt) >> pc.log2B))
+                               : read_row(pc, r0 + cnt);
+      bad |= nxt <= P[pidx(cnt - 1)];
     }
-    if (lane == 0) seg_info[item] = c | (last << 16);
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(err, err_bit(MS_E_INVALID));
     __syncwarp();
   }
 }
 
-cudaError_t launch_semi_mask(const ColView& pos1, const ColView& keys, uint64_t row_offset, const uint64_t* bitmap,
-                             uint64_t bits_n, uint32_t* bits, uint32_t* seg_info, uint32_t* err, cudaStream_t s) {
+cudaError_t launch_semi_rows(const ColView& pos1, const ColView& keys, uint64_t row_offset, const uint64_t* bitmap,
+                             uint64_t bitmap_bits, uint32_t* mask, uint32_t* err, cudaStream_t s) {
   const uint64_t n_items = (pos1.n + kSegRows - 1) / kSegRows;
   if (!n_items) return cudaSuccess;
   const int warps = 4;
   const size_t smem = (size_t)warps * tile_slots(kSegRows) * 8;
-  set_smem_once((const void*)semi_mask_kernel, smem);
-  int per_sm = 0;
-  per_sm = occupancy_cached((const void*)semi_mask_kernel, warps * 32, smem);
+  set_smem_once((const void*)semi_rows_kernel, smem);
+  int per_sm = occupancy_cached((const void*)semi_rows_kernel, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)per_sm * num_sms();
   const uint64_t need = (n_items + warps - 1) / warps;
   if (need < grid) grid = need;
-  ProfScope prof_("semi_mask", s);
-  semi_mask_kernel<<<(int)grid, warps * 32, smem, s>>>(ProjectSource<4>{pos1, keys, row_offset, 1u}, pos1.n, bitmap,
-                                                      bits_n, bits, seg_info, err);
+  ProfScope prof_("semi_rows", s);
+  semi_rows_kernel<<<(int)grid, warps * 32, smem, s>>>(ProjectSource<4>{pos1, keys, row_offset, 1u}, pos1.n,
+                                                       SemiRowSet{bitmap, bitmap_bits, row_offset, keys.n, mask},
+                                                       err);
   return cudaGetLastError();
 }
+
 
 // select positions in a format other than DELTA_BP (items <= 512): MaskSource into
 // the slot encoder; block formats then scan the widths and copy (no look-back)

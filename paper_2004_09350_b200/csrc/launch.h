@@ -165,8 +165,10 @@ cudaError_t launch_join_probe(const ColView& probe, uint32_t* state, uint64_t* k
 cudaError_t launch_calc(const ColView& a, const ColView& b, int op, uint64_t* out, cudaStream_t s);
 // K7 (encode.cu): mask over pos1's ranks of the positions whose key is in the bitmap (select mask
 // layout: 16 words + one seg_info per 512 ranks); pos1 DELTA_BP{512} or O(1) formats, keys O(1) formats
-cudaError_t launch_semi_mask(const ColView& pos1, const ColView& keys, uint64_t row_offset, const uint64_t* bitmap,
-                             uint64_t bits_n, uint32_t* bits, uint32_t* seg_info, uint32_t* err, cudaStream_t s);
+// K7, row space: surviving positions as bits of a zeroed mask over the keys' rows
+cudaError_t launch_semi_rows(const ColView& pos1, const ColView& keys, uint64_t row_offset, const uint64_t* bitmap,
+                             uint64_t bitmap_bits, uint32_t* mask, uint32_t* err, cudaStream_t s);
+
 // RLE encoding from a column source (morph into RLE): counts per 2048-row tile (first_last: 2 u64 per
 // tile), then, after the scan of the counts, (value, start) of every run
 cudaError_t launch_rle_count_col(const ColView& c, uint32_t* counts, uint64_t* first_last, cudaStream_t s);

@@ -84,8 +84,19 @@ struct ProjectSource {
   ColView data;
   uint64_t row_offset;
   uint32_t prefetch;  // bulk-prefetch the data window into L2 before gathering
+  // the gathered value of rank i (position p) goes to f(i, p, v); load() stores it in P
+  struct Store {
+    uint64_t* P;
+    __device__ __forceinline__ void operator()(uint32_t i, uint64_t, uint64_t v) const { P[pidx(i)] = v; }
+  };
   __device__ __forceinline__ void load(uint32_t item, uint64_t r0, uint32_t cnt, uint64_t* P, uint32_t lane,
                                        uint32_t* err) const {
+    load_with(item, r0, cnt, P, lane, err, Store{P});
+  }
+  // positions of ranks [r0, r0 + cnt) into P, then each one's data value to f
+  template <class F>
+  __device__ __forceinline__ void load_with(uint32_t item, uint64_t r0, uint32_t cnt, uint64_t* P, uint32_t lane,
+                                            uint32_t* err, const F& f) const {
     // ---- positions
     if (pos.format == MS_DELTA_BP && r0 + cnt <= (pos.nb << pos.log2B)) {  // block-aligned: B == G (host checks)
       const uint64_t b = r0 >> pos.log2B;
@@ -164,11 +175,12 @@ struct ProjectSource {
         }
       }
       for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * BATCH) {
-        uint64_t v[BATCH];
+        uint64_t v[BATCH], pp[BATCH];
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
           const uint64_t p = i < cnt ? P[pidx(i)] : row_offset;
+          pp[q] = p;
           const bool ok = p >= row_offset && p - row_offset < data.n;
           if (i < cnt && !ok) atomicOr(err, err_bit(MS_E_RANGE));
           const uint64_t r = ok ? p - row_offset : 0;
@@ -197,7 +209,7 @@ struct ProjectSource {
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
-          if (i < cnt) P[pidx(i)] = v[q];
+          if (i < cnt) f(i, pp[q], v[q]);
         }
       }
     } else if (data.format == MS_STATIC_BP || data.format == MS_UNCOMPR) {
@@ -216,11 +228,12 @@ struct ProjectSource {
                        : "memory");
       }
       for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * BATCH) {
-        uint64_t v[BATCH];
+        uint64_t v[BATCH], pp[BATCH];
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
           const uint64_t p = i < cnt ? P[pidx(i)] : row_offset;
+          pp[q] = p;
           const bool ok = p >= row_offset && p - row_offset < data.n;
           if (i < cnt && !ok) atomicOr(err, err_bit(MS_E_RANGE));
           const uint64_t r = ok ? p - row_offset : 0;
@@ -229,7 +242,7 @@ struct ProjectSource {
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
           const uint32_t i = i0 + q * 32 + lane;
-          if (i < cnt) P[pidx(i)] = v[q];
+          if (i < cnt) f(i, pp[q], v[q]);
         }
       }
     } else {
@@ -238,7 +251,7 @@ struct ProjectSource {
         uint64_t v = 0;
         if (p < row_offset || p - row_offset >= data.n) atomicOr(err, err_bit(MS_E_RANGE));
         else v = read_row(data, p - row_offset);
-        P[pidx(i)] = v;
+        f(i, p, v);
       }
     }
     __syncwarp();

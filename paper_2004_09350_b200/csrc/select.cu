@@ -201,29 +201,33 @@ __global__ void __launch_bounds__(256) rle_mask_kernel(ColView c, Pred pred, uin
   }
 }
 
-// per 512-row segment: count | (1-based last matching row << 16), from the mask
+// per 512-row segment: count | (1-based last matching row << 16), from the mask;
+// a warp takes eight segments per step (lane l: 16 bytes, words 4l .. 4l + 3)
 __global__ void __launch_bounds__(256) seg_info_kernel(const uint32_t* bits, uint64_t NS, uint32_t* seg_info) {
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint64_t sg2 = gw; sg2 * 2 < NS; sg2 += nw) {  // a warp takes two segments (32 words)
-    const uint64_t sg = sg2 * 2 + (lane >> 4);
-    const uint32_t m = sg < NS ? bits[sg * kSegWords + (lane & 15)] : 0u;
-    uint32_t cnt = __popc(m);
-    uint32_t last = m ? (lane & 15) * 32 + 32 - __clz(m) : 0u;
+  const uint32_t lane = threadIdx.x & 31, q = lane & 3;
+  for (uint64_t s8 = gw; s8 * 8 < NS; s8 += nw) {
+    const uint64_t sg = s8 * 8 + (lane >> 2);
+    uint4 m = make_uint4(0u, 0u, 0u, 0u);
+    if (sg < NS) m = __ldg(reinterpret_cast<const uint4*>(bits + sg * kSegWords) + q);
+    uint32_t cnt = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+    const uint32_t wb = q * 128;  // the lane's first row in the segment
+    uint32_t last = m.w ? wb + 128 - __clz(m.w)
+                        : m.z ? wb + 96 - __clz(m.z) : m.y ? wb + 64 - __clz(m.y) : m.x ? wb + 32 - __clz(m.x) : 0u;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
+    for (int o = 2; o > 0; o >>= 1) {
       cnt += __shfl_xor_sync(kFull, cnt, o);
       last = max(last, __shfl_xor_sync(kFull, last, o));
     }
-    if (sg < NS && (lane & 15) == 0) seg_info[sg] = cnt | (last << 16);
+    if (sg < NS && q == 0) seg_info[sg] = cnt | (last << 16);
   }
 }
 
 cudaError_t launch_seg_info(const uint32_t* bits, uint64_t NS, uint32_t* seg_info, cudaStream_t s) {
   if (!NS) return cudaSuccess;
-  uint64_t g2 = (NS + 15) / 16;
-  if (g2 > (uint64_t)num_sms() * 16) g2 = num_sms() * 16;
+  uint64_t g2 = (NS + 63) / 64;  // 8 warps x 8 segments per CTA step
+  if (g2 > (uint64_t)num_sms() * 8) g2 = num_sms() * 8;
   ProfScope prof_("seg_info", s);
   seg_info_kernel<<<(int)g2, 256, 0, s>>>(bits, NS, seg_info);
   return cudaGetLastError();
@@ -244,11 +248,7 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    uint64_t g2 = (NS + 15) / 16;
-    if (g2 > (uint64_t)num_sms() * 16) g2 = num_sms() * 16;
-    ProfScope prof_("seg_info", s);
-    seg_info_kernel<<<(int)g2, 256, 0, s>>>(bits, NS, seg_info);
-    return cudaGetLastError();
+    return launch_seg_info(bits, NS, seg_info, s);
   }
   // fast path: UNCOMPR, STATIC_BP, DYN_BP / FOR_BP with B >= 512, on full 512-row segments
   int kind = -1;

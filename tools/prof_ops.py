@@ -91,6 +91,29 @@ def c4():
     prof("grouped sum", lambda: ms.agg_sum_grouped(gid, m1p, 1000))
 
 
+def c4f():  # the fused D-16 chain (K7 semi-join), operator by operator
+    n = 600_000_000
+    Dm = synth.D4
+    bm = torch.from_numpy(synth.bitmap_c4().view("int64")).cuda()
+    gattr = ms.compress(synth.gen_torch("c4.gattr", Dm[3]), ms.static_bp(10))
+    k0 = ms.compress(synth.gen_torch("c4.k0", n), ms.static_bp(12))
+    k1 = ms.compress(synth.gen_torch("c4.k1", n), ms.static_bp(18))
+    k3 = ms.compress(synth.gen_torch("c4.k3", n), ms.static_bp(17))
+    m1 = ms.compress(synth.gen_torch("c4.m1", n), ms.dyn_bp(512))
+    pos1 = ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512))
+    prof("select k0", lambda: ms.select(k0, ms.BETWEEN, 0, 365, out_fmt=ms.delta_bp(512)))
+    pos2 = ms.semijoin(k1, pos1, bm, Dm[1])
+    prof("semijoin k1 @ pos1", lambda: ms.semijoin(k1, pos1, bm, Dm[1]))
+    prof("project m1 @ pos2 -> DYN", lambda: ms.project(m1, pos2, 0, ms.dyn_bp(512)))
+    k3p = ms.project(k3, pos2, 0, ms.static_bp(17))
+    prof("project k3 @ pos2 -> STATIC 17", lambda: ms.project(k3, pos2, 0, ms.static_bp(17)))
+    gid = ms.project(gattr, k3p, 0, ms.static_bp(10))
+    prof("project gattr @ k3' -> STATIC 10", lambda: ms.project(gattr, k3p, 0, ms.static_bp(10)))
+    m1p = ms.project(m1, pos2, 0, ms.dyn_bp(512))
+    prof("grouped sum", lambda: ms.agg_sum_grouped(gid, m1p, 1000))
+    print(f"pos1 {pos1.n} pos2 {pos2.n}", flush=True)
+
+
 def c2():
     n = 1 << 28
     X = ms.compress(synth.gen_torch("c2.X", n), ms.dyn_bp(512))
