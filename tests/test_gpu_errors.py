@@ -102,3 +102,35 @@ def test_release_on_other_stream():
         got = ms.to_u64_numpy(ms.decompress(pos))
         assert np.array_equal(got, expect)
         del junk
+
+
+@pytest.mark.parametrize("kind", ["unsorted", "duplicate", "across_blocks"])
+def test_semijoin_rejects_unsorted_positions(kind):
+    """ms_semijoin requires strictly increasing positions (include/ms.h): the
+    fused kernel flags MS_E_INVALID for a block that is not, or whose successor
+    does not start after it; sorted positions in the same formats stay exact."""
+    import torch
+    ms = get_ms()
+    rng = np.random.default_rng(11)
+    n = 20_000
+    keys = rng.integers(0, 1000, n).astype(np.uint64)
+    K = ms.compress(to_torch(keys), ms.static_bp(10))
+    bm = np.zeros(16, np.uint64)
+    bm[:8] = 0x5555555555555555
+    bmt = torch.from_numpy(bm.view(np.int64)).cuda()
+    p = np.sort(rng.choice(n, 3000, replace=False)).astype(np.uint64)
+    bad = p.copy()
+    if kind == "unsorted":
+        bad[10], bad[11] = bad[11], bad[10]
+    elif kind == "duplicate":
+        bad[100] = bad[99]
+    else:  # block 1 starts before block 0 ends
+        bad[512] = bad[511] - 1 if bad[511] - 1 > bad[510] else bad[511]
+    P = ms.compress(to_torch(bad), ms.uncompr())
+    with pytest.raises(ms.MsError) as e:
+        ms.semijoin(K, P, bmt, 1000)
+    assert e.value.code == 1  # MS_E_INVALID
+    good = ms.compress(to_torch(p), ms.uncompr())
+    got = ms.to_u64_numpy(ms.decompress(ms.semijoin(K, good, bmt, 1000, out_fmt=ms.uncompr())))
+    keep = (keys[p.astype(np.int64)] < 512) & (keys[p.astype(np.int64)] % 2 == 0)
+    assert np.array_equal(got, p[keep])
