@@ -9,6 +9,8 @@
 
 namespace ms {
 
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 // ------------------------------------------------- select output encoder
 template <class Src>
 static cudaError_t run_warp_encode(const Src& src, const PosEnc& e0, uint64_t* status, uint32_t* ticket,
@@ -128,10 +130,12 @@ cudaError_t launch_project_warp(const ColView& pos, const ColView& data, uint64_
 // positions project (which decoded every pos1 block again). Requires pos1
 // strictly increasing (every positions column the library produces); a block
 // that is not, or whose successor does not start after it, flags MS_E_INVALID.
+// A surviving position p (its key v in the bitmap) sets bit p - row_offset of the
+// zeroed row mask.
 struct SemiRowSet {
   const uint64_t* bitmap;
   uint64_t bits_n, row_offset, n_rows;
-  uint32_t* mask;  // zeroed, 1 bit per row of the keys
+  uint32_t* mask;
   __device__ __forceinline__ void operator()(uint32_t, uint64_t p, uint64_t v) const {
     const uint64_t r = p - row_offset;
     if (p < row_offset || r >= n_rows) return;  // MS_E_RANGE raised by the loader
@@ -171,6 +175,8 @@ cudaError_t launch_semi_rows(const ColView& pos1, const ColView& keys, uint64_t 
                              uint64_t bitmap_bits, uint32_t* mask, uint32_t* err, cudaStream_t s) {
   const uint64_t n_items = (pos1.n + kSegRows - 1) / kSegRows;
   if (!n_items) return cudaSuccess;
+  const ProjectSource<4> src{pos1, keys, row_offset, 1u};
+  const SemiRowSet set{bitmap, bitmap_bits, row_offset, keys.n, mask};
   const int warps = 4;
   const size_t smem = (size_t)warps * tile_slots(kSegRows) * 8;
   set_smem_once((const void*)semi_rows_kernel, smem);
@@ -180,9 +186,7 @@ cudaError_t launch_semi_rows(const ColView& pos1, const ColView& keys, uint64_t 
   const uint64_t need = (n_items + warps - 1) / warps;
   if (need < grid) grid = need;
   ProfScope prof_("semi_rows", s);
-  semi_rows_kernel<<<(int)grid, warps * 32, smem, s>>>(ProjectSource<4>{pos1, keys, row_offset, 1u}, pos1.n,
-                                                       SemiRowSet{bitmap, bitmap_bits, row_offset, keys.n, mask},
-                                                       err);
+  semi_rows_kernel<<<(int)grid, warps * 32, smem, s>>>(src, pos1.n, set, err);
   return cudaGetLastError();
 }
 
@@ -284,7 +288,6 @@ cudaError_t launch_project_slots(const ColView& pos, const ColView& data, uint64
   return cudaGetLastError();
 }
 
-static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 bool project_stream_supported(const ColView& pos, const ColView& data, const PosEnc& e) {
   const bool block_out = e.format == MS_DYN_BP || e.format == MS_FOR_BP || e.format == MS_DELTA_BP;
