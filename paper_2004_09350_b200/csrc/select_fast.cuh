@@ -133,12 +133,32 @@ __device__ __forceinline__ uint32_t lane_rows(const uint32_t* __restrict__ p, co
           else z = (__funnelshift_r(r[q], r[q + 1], sh) & hi) == 0u;
           if (z) m |= 1u << i;  // (a predicated OR with a constant)
         }
+      } else if (sp >= cmask) {
+        m = ~0u;  // every code of the block matches
       } else {
+        // general interval [a, a + sp] (inside [0, 2^W)): each code is read top-aligned,
+        // ct = c * 2^K + g with K = 32 - W and g < 2^K the bits of the code below it,
+        // so c - a <= sp  <=>  ct - a * 2^K <= T = sp * 2^K + 2^K - 1 (a code below a
+        // wraps past T). The test is the carry of (ct - a * 2^K) + ~T (set iff the row
+        // does NOT match), shifted into the inverted mask by addc: three instructions
+        // per row (shift-subtract, add with carry-out, add with carry-in), no mask
+        // extraction, no compare-and-select.
+        constexpr int K = 32 - W;
+        const uint32_t at = a << K;
+        const uint32_t nT = ~((sp << K) | ((1u << K) - 1u));
+        uint32_t mi = 0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const uint32_t c = (uint32_t)code_at<W>(r, i);
-          if ((c - a) <= sp) m |= 1u << i;
+        for (int i = 31; i >= 0; --i) {  // row 31 first: addc doubles the mask each row
+          const int bit = i * W, q = bit >> 5, sh = bit & 31;
+          uint32_t ct;
+          if (sh + W <= 32) ct = r[q] << (32 - sh - W);
+          else ct = __funnelshift_l(r[q], r[q + 1], 64 - sh - W);
+          const uint32_t d = ct - at;
+          asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %3;\n\t}"
+              : "=r"(mi)
+              : "r"(d), "r"(nT), "r"(mi));
         }
+        m = ~mi;
       }
       if (ng) m = ~m;  // the negated predicates, once per 32 rows
     } else {
