@@ -260,7 +260,8 @@ cudaError_t launch_select(const ColView& c, const PredSpec& p, uint32_t* bits, u
     ns_fast = (c.nb << c.log2B) / kSegRows;
   }
   if (kind >= 0 && ns_fast) {
-    FastPred fp{p.lo, p.span, p.neg, (uint32_t)p.is_bitmap, p.bitmap, p.bitmap_bits};
+    FastPred fp{p.lo, p.span, p.neg, (uint32_t)p.is_bitmap, p.bitmap, p.bitmap_bits, {}, 0};
+    fast_pred_table(fp);
     auto pick = [&](auto k, int stages, int warps_per_cta, int bufu32 = kPairBufWide) {
       const size_t smem = (size_t)warps_per_cta * stages * bufu32 * 4;
       set_smem_once((const void*)k, smem);

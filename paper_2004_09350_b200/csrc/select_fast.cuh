@@ -16,13 +16,19 @@ constexpr int kBufU32 = 1024 + 8;        // 4 KiB (512 rows x 64 bit) + padding 
 
 enum : int { FAST_UNCOMPR = 0, FAST_STATIC = 1, FAST_BLOCK = 2 };
 
-// predicate passed to the fast kernel: keep = ((v - lo) <= span) != neg, or bitmap
+// predicate passed to the fast kernel: keep = ((v - lo) <= span) != neg, or bitmap.
+// iv[W] = the code-domain interval (a, s) of code_interval for codes of width W
+// and reference 0 (STATIC_BP, DYN_BP: the common case), neg in bit W of iv_neg;
+// filled on the host by fast_pred_table() so a lane reads it from the parameter
+// bank at a compile-time index instead of translating the constant per 32 rows.
 struct FastPred {
   uint64_t lo, span;
   uint32_t neg;
   uint32_t is_bitmap;
   const uint64_t* bitmap;
   uint64_t bits;
+  uint32_t iv[33][2];
+  uint64_t iv_neg;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -36,7 +42,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Code-domain translation of the range predicate for codes c in [0, 2^W), W <= 32,
 // with values v = ref + c: returns (a, s, neg) such that
 // keep(c) = ((c - a) mod 2^32 <= s) != neg.
-__device__ __forceinline__ void code_interval(uint64_t lo, uint64_t span, uint32_t neg0, uint64_t ref, uint32_t W,
+__host__ __device__ __forceinline__ void code_interval(uint64_t lo, uint64_t span, uint32_t neg0, uint64_t ref, uint32_t W,
                                               uint32_t& a, uint32_t& s, uint32_t& neg) {
   const uint64_t M1 = W >= 64 ? ~0ull : ((1ull << W) - 1);  // largest code
   const uint64_t d = lo - ref;                              // matching codes: (c - d) mod 2^64 <= span
@@ -56,6 +62,19 @@ __device__ __forceinline__ void code_interval(uint64_t lo, uint64_t span, uint32
     const uint64_t chi = (d - 1) < M1 ? (d - 1) : M1;
     a = (uint32_t)(e + 1); s = (uint32_t)(chi - (e + 1)); neg = neg0 ^ 1u;
   }
+}
+
+// the per-width table of FastPred (reference 0)
+inline void fast_pred_table(FastPred& fp) {
+  fp.iv_neg = 0;
+  for (uint32_t W = 1; W <= 32; ++W) {
+    uint32_t a, sp, ng;
+    code_interval(fp.lo, fp.span, fp.neg, 0, W, a, sp, ng);
+    fp.iv[W][0] = a;
+    fp.iv[W][1] = sp;
+    fp.iv_neg |= (uint64_t)(ng & 1u) << W;
+  }
+  fp.iv[0][0] = fp.iv[0][1] = 0;
 }
 
 // ---- lane-consecutive core: lane l of a half-warp owns rows 32l .. 32l+31 of
@@ -118,7 +137,13 @@ __device__ __forceinline__ uint32_t lane_rows(const uint32_t* __restrict__ p, co
       }
     } else if constexpr (W <= 32) {
       uint32_t a, sp, ng;
-      code_interval(pr.lo, pr.span, pr.neg, ref, W, a, sp, ng);
+      if (ref == 0) {
+        a = pr.iv[W][0];
+        sp = pr.iv[W][1];
+        ng = (uint32_t)(pr.iv_neg >> W) & 1u;
+      } else {
+        code_interval(pr.lo, pr.span, pr.neg, ref, W, a, sp, ng);
+      }
       constexpr uint32_t cmask = W >= 32 ? 0xffffffffu : ((1u << (W & 31)) - 1u);
       if (a == 0 && (sp & (sp + 1)) == 0 && sp < cmask) {
         // prefix interval [0, 2^k): a code matches iff its bits k..W-1 are zero — one
