@@ -48,32 +48,39 @@ struct Ctx {
 };
 
 // One scratch allocation per op, carved into 256-byte aligned regions.
+// Per-op scratch from the stream's caching allocator. Regions asked zeroed are laid
+// out together after the others, so commit() clears all of them with ONE memset
+// (one launch per op instead of one per region); their offsets carry kZeroTag
+// until at() maps them (offset arithmetic on a returned offset stays valid).
 struct Scratch {
+  static constexpr uint64_t kZeroTag = 1ull << 62;
   const Ctx& ctx;
-  std::vector<uint64_t> zero_off, zero_len;
-  uint64_t size = 0;
+  uint64_t size = 0, zsize = 0, zstart = 0;
   char* base = nullptr;
   explicit Scratch(const Ctx& c) : ctx(c) {}
   ~Scratch() { ctx.free(base); }
   uint64_t add(uint64_t bytes, bool zero) {
-    uint64_t off = size;
-    size = align_up(size + (bytes ? bytes : 8));
+    const uint64_t b = bytes ? bytes : 8;
     if (zero) {
-      zero_off.push_back(off);
-      zero_len.push_back(bytes ? bytes : 8);
+      const uint64_t off = zsize;
+      zsize = align_up(zsize + b);
+      return kZeroTag | off;
     }
+    const uint64_t off = size;
+    size = align_up(size + b);
     return off;
   }
   bool commit() {
-    base = (char*)ctx.alloc(size ? size : kAlign);
+    zstart = align_up(size);
+    const uint64_t total = zstart + zsize;
+    base = (char*)ctx.alloc(total ? total : kAlign);
     if (!base) return false;
-    // coalesce the zero regions into one memset when they are dense enough
-    for (size_t i = 0; i < zero_off.size(); ++i)
-      if (cudaMemsetAsync(base + zero_off[i], 0, zero_len[i], ctx.s) != cudaSuccess) return false;
-    return true;
+    return !zsize || cudaMemsetAsync(base + zstart, 0, zsize, ctx.s) == cudaSuccess;
   }
   template <class T>
-  T* at(uint64_t off) const { return reinterpret_cast<T*>(base + off); }
+  T* at(uint64_t off) const {
+    return reinterpret_cast<T*>(base + ((off & kZeroTag) ? zstart + (off & ~kZeroTag) : off));
+  }
 };
 
 ms_status status_from_bits(uint32_t bits) {
@@ -542,7 +549,8 @@ ms_status positions_from_mask(const Ctx& ctx, uint32_t* bits, uint32_t* seg_info
   const bool wscan = pos_delta || pos_slots;
   const uint64_t o_wk = wscan ? sc.add(4 * (items_max + 1), false) : 0;
   const uint64_t o_cwx = wscan ? sc.add(8 * (items_max + 2), false) : 0;
-  const uint64_t o_dlc = pos_delta ? sc.add(4 * (items_max + 2), true) : 0;  // deferred blocks: count, entries
+  const uint64_t o_dlz = pos_delta ? sc.add(8, true) : 0;                      // deferred blocks: count
+  const uint64_t o_dlc = pos_delta ? sc.add(4 * (items_max + 1), false) : 0;    // deferred blocks: entries
   const uint64_t o_st3 = wscan ? sc.add(8 * ((items_max + kChunk - 1) / kChunk + 1), true) : 0;
   const uint64_t o_tk3 = wscan ? sc.add(8, true) : 0;
   if (!sc.commit()) return MS_E_NOMEM;
@@ -633,7 +641,7 @@ ms_status positions_from_mask(const Ctx& ctx, uint32_t* bits, uint32_t* seg_info
         pos_delta && f.format == MS_DELTA_BP
             ? launch_positions_delta(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset,
                                      sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx), sc.at<uint64_t>(o_st3),
-                                     sc.at<uint32_t>(o_tk3), slots, slot_words, sc.at<uint32_t>(o_dlc), err, ctx.s)
+                                     sc.at<uint32_t>(o_tk3), slots, slot_words, sc.at<uint32_t>(o_dlz), sc.at<uint32_t>(o_dlc), err, ctx.s)
         : pos_slots
             ? launch_positions_slots(pe, bits, NS, sc.at<uint64_t>(o_gs), row_offset, slots,
                                      slot_words, sc.at<uint32_t>(o_wk), sc.at<uint64_t>(o_cwx),

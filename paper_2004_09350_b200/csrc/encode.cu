@@ -60,7 +60,7 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
 
 cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                                    uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
-                                   uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* dlist,
+                                   uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words, uint32_t* dcount, uint32_t* dlist,
                                    uint32_t* err, cudaStream_t s) {
   const uint64_t n_items = (e.n_out + e.G - 1) / e.G;
   const uint64_t n_full = e.n_out / e.G;
@@ -85,14 +85,14 @@ cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64
       if (dense) {
         const int grid = grid_for(pos_slot_kernel<kPdDense>, smem, n_items);
         pos_slot_kernel<kPdDense><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items,
-                                                                   slots, slot_words, wk, dlist, err);
+                                                                   slots, slot_words, wk, dcount, dlist, err);
         pos_slot_kernel<kPdDeferredOnly><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e,
-                                                                          n_items, slots, slot_words, wk, dlist, err);
+                                                                          n_items, slots, slot_words, wk, dcount, dlist, err);
         count_launch();
       } else {
         const int grid = grid_for(pos_slot_kernel<kPdAll>, smem, n_items);
         pos_slot_kernel<kPdAll><<<grid, kPdWarps * 32, smem, s>>>(bits, n_words, gstart, row_offset, e, n_items,
-                                                                 slots, slot_words, wk, dlist, err);
+                                                                 slots, slot_words, wk, dcount, dlist, err);
       }
     }
     cudaError_t r = cudaGetLastError();

@@ -86,7 +86,8 @@ cudaError_t launch_positions(const PosEnc& e, const uint32_t* bits, uint64_t NS,
 cudaError_t launch_positions_delta(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,
                                    uint64_t row_offset, uint32_t* wk, uint64_t* cwx, uint64_t* scan_status,
                                    uint32_t* scan_ticket, uint64_t* slots, uint32_t slot_words,
-                                   uint32_t* dlist,  // zeroed [0]: count, then the deferred blocks
+                                   uint32_t* dcount,  // zeroed: the number of deferred blocks
+                                   uint32_t* dlist,   // the deferred blocks
                                    uint32_t* err, cudaStream_t s);
 // select positions in other formats (items <= 512) through the slot encoder (+ scan, copy for block formats)
 cudaError_t launch_positions_slots(const PosEnc& e, const uint32_t* bits, uint64_t NS, const uint64_t* gstart,

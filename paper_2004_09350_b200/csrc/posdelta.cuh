@@ -440,7 +440,7 @@ __device__ __forceinline__ void pd_store_slot(uint64_t item, uint32_t w, uint64_
 }
 
 // MODE kPdDense (B = 512): pd_item512 only; a block whose span does not fit (and
-// the block before the last) is appended to dlist (dlist[0]: count) and left to a
+// the block before the last) is appended to dlist (*dcount: count) and left to a
 // kPdDeferredOnly launch, whose warps take the listed blocks one each. The walk's
 // registers stay out of the fast path. kPdAll: the walk for every block.
 constexpr int kPdAll = 0, kPdDense = 1, kPdDeferredOnly = 2;
@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
                                                                  const uint64_t* __restrict__ gstart,
                                                                  uint64_t row_offset, PosEnc e, uint64_t n_items,
                                                                  uint64_t* __restrict__ slots, uint32_t slot_words,
-                                                                 uint32_t* __restrict__ wk, uint32_t* dlist,
-                                                                 uint32_t* err) {
+                                                                 uint32_t* __restrict__ wk, uint32_t* dcount,
+                                                                 uint32_t* dlist, uint32_t* err) {
   extern __shared__ __align__(16) uint32_t pd_sm[];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* stage = pd_sm + (size_t)wid * kPdWarpU32;
@@ -482,9 +482,9 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
   const uint64_t nwarps = (uint64_t)gridDim.x * kPdWarps;
   const uint64_t gw = (uint64_t)blockIdx.x * kPdWarps + wid;
   if (MODE == kPdDeferredOnly) {  // the listed blocks, one per warp
-    const uint32_t nd = *reinterpret_cast<volatile uint32_t*>(dlist);
+    const uint32_t nd = *reinterpret_cast<volatile uint32_t*>(dcount);
     for (uint64_t i = gw; i < nd; i += nwarps) {
-      const uint64_t item = __ldg(dlist + 1 + i);
+      const uint64_t item = __ldg(dlist + i);
       pd_walk_block(bits, n_words, __ldg(gstart + item) - row_offset, item, row_offset, e, slots, slot_words, wk,
                     stage, lane, err);
     }
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kPdWarps * 32, 5) pos_slot_kernel(const uint32
         const uint32_t w = pd_item512(bits, row0, rowE, reinterpret_cast<uint16_t*>(stage), lane, err);
         pd_store_slot(item, w, row0 + row_offset, e, slots, slot_words, wk, stage, lane, err);
       } else if (lane == 0) {
-        dlist[1 + atomicAdd(dlist, 1u)] = (uint32_t)item;
+        dlist[atomicAdd(dcount, 1u)] = (uint32_t)item;
       }
     } else {
       pd_walk_block(bits, n_words, row0, item, row_offset, e, slots, slot_words, wk, stage, lane, err);
