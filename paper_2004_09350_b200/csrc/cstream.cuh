@@ -8,8 +8,9 @@
 // tiles; warp 0 issues one TMA bulk copy per tile (16 KiB) into stage li % 10
 // (mbarrier complete_tx); consumer pair li % 10 (two warps, no CTA barrier):
 //   pass 1  per block, warp h takes the 32-row groups h, h + 2, ... (row 32g +
-//           lane): the extremes (DELTA: of d = v - v_prev, d_0 = 0, D-6) reduced
-//           across the warp and combined in shared memory;
+//           lane): FOR: the extremes; DYN / DELTA: the OR of the values (DELTA: of
+//           d = v - v_prev, d_0 = 0, D-6) — ebw(max) = ebw(OR) — reduced across
+//           the warp (redux) and combined in shared memory;
 //   widths  lane b: w_b (DYN: ebw(max), FOR: ebw(max - min), DELTA: ebw(max d)),
 //           exclusive prefix over the tile's blocks -> bw, ref, slot offsets;
 //   pack    thread t of the pair builds u32 words t, t + 64, ... of each block
@@ -151,28 +152,45 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     // pass 1: warp h takes the 32-row groups h, h + 2, ...; per block: the extremes (DELTA:
     // of the differences v - v_prev, d_0 = 0), reduced across the warp, combined in shared memory
     for (uint32_t b = 0; b < nbc; ++b) {
-      uint64_t lo = ~0ull, hi = 0;
-      const uint32_t i1 = (b + 1) << lg;
+      const uint32_t i0 = (b << lg) + h * 32 + lane, i1 = (b + 1) << lg;
+      if (is_for) {  // FOR: the extremes themselves (ref = min, w = ebw(max - min))
+        uint64_t lo = ~0ull, hi = 0;
 #pragma unroll 4
-      for (uint32_t i = (b << lg) + h * 32 + lane; i < i1; i += 32 * kCsPair) {
-        const uint64_t v = V[i];
-        if (is_delta) {
-          const uint64_t d = (i & (B - 1)) ? v - V[i - 1] : 0ull;
-          hi = d > hi ? d : hi;
-        } else {
+        for (uint32_t i = i0; i < i1; i += 32 * kCsPair) {
+          const uint64_t v = V[i];
           lo = v < lo ? v : lo;
           hi = v > hi ? v : hi;
         }
-      }
 #pragma unroll
-      for (int q = 16; q > 0; q >>= 1) {
-        const uint64_t a2 = __shfl_xor_sync(kFull, lo, q), b2 = __shfl_xor_sync(kFull, hi, q);
-        lo = a2 < lo ? a2 : lo;
-        hi = b2 > hi ? b2 : hi;
-      }
-      if (lane == 0) {
-        if (!is_delta) atomicMin(&W.lo[b], (unsigned long long)lo);
-        atomicMax(&W.hi[b], (unsigned long long)hi);
+        for (int q = 16; q > 0; q >>= 1) {
+          const uint64_t a2 = __shfl_xor_sync(kFull, lo, q), b2 = __shfl_xor_sync(kFull, hi, q);
+          lo = a2 < lo ? a2 : lo;
+          hi = b2 > hi ? b2 : hi;
+        }
+        if (lane == 0) {
+          atomicMin(&W.lo[b], (unsigned long long)lo);
+          atomicMax(&W.hi[b], (unsigned long long)hi);
+        }
+      } else {  // DYN / DELTA: only ebw(max) is needed, and ebw(max) = ebw(OR): one OR per row
+        uint32_t ol = 0, oh = 0;
+        if (is_delta) {
+#pragma unroll 4
+          for (uint32_t i = i0; i < i1; i += 32 * kCsPair) {
+            const uint64_t d = (i & (B - 1)) ? V[i] - V[i - 1] : 0ull;
+            ol |= (uint32_t)d;
+            oh |= (uint32_t)(d >> 32);
+          }
+        } else {
+#pragma unroll 4
+          for (uint32_t i = i0; i < i1; i += 32 * kCsPair) {
+            const uint2 v = *reinterpret_cast<const uint2*>(V + i);
+            ol |= v.x;
+            oh |= v.y;
+          }
+        }
+        ol = __reduce_or_sync(kFull, ol);
+        oh = __reduce_or_sync(kFull, oh);
+        if (lane == 0) atomicOr(&W.hi[b], ((unsigned long long)oh << 32) | ol);
       }
     }
     cs_bar(p);
