@@ -5,8 +5,8 @@
 // __syncthreads and ~6,700 warp instructions per tile).
 //
 // compress_stream_kernel: persistent, one CTA per SM, each CTA a contiguous run of
-// tiles; warp 0 issues one TMA bulk copy per tile (16 KiB) into stage li % 10
-// (mbarrier complete_tx); consumer pair li % 10 (two warps, no CTA barrier):
+// tiles; warp 0 issues one TMA bulk copy per tile (16 KiB) into stage li % 12
+// (mbarrier complete_tx); consumer pair li % 12 (two warps, no CTA barrier):
 //   pass 1  per block, warp h takes the 32-row groups h, h + 2, ... (row 32g +
 //           lane): FOR: the extremes; DYN / DELTA: the OR of the values (DELTA: of
 //           d = v - v_prev, d_0 = 0, D-6) — ebw(max) = ebw(OR) — reduced across
@@ -26,13 +26,14 @@
 
 namespace ms {
 
-constexpr int kCsStages = 10;
+constexpr int kCsStages = 12;
 constexpr int kCsPair = 2;  // consumer warps per stage
 constexpr int kCsThreads = (1 + kCsPair * kCsStages) * 32;
 
 struct CsPair {  // per stage: the tile's block statistics
   unsigned long long lo[kChunk / 128], hi[kChunk / 128];
   uint32_t w[kChunk / 128], ex[kChunk / 128];
+  uint32_t wmax, pad_[3];  // the tile's largest block width
 };
 
 __host__ __device__ constexpr size_t cs_smem_bytes() {
@@ -88,6 +89,57 @@ __device__ __forceinline__ void cs_pack_dispatch(uint32_t w, const uint64_t* cb,
     MS_CS_CASE(57) MS_CS_CASE(58) MS_CS_CASE(59) MS_CS_CASE(60) MS_CS_CASE(61) MS_CS_CASE(62) MS_CS_CASE(63)
     MS_CS_CASE(64)
 #undef MS_CS_CASE
+    default:
+      break;
+  }
+}
+
+
+// ---- narrow blocks (w <= 16): the word-per-thread builder reads the code at the
+// start of each word, 32 / W elements apart, so the lanes of a half-warp fall on
+// W (odd W) or fewer bank pairs (ncu at c3, DELTA, W ~ 5: 4.4-way conflicts, 62 % of
+// the shared-load wavefronts, the L1 pipe at 88 %). Instead the tile's codes are
+// staged once as u32 at 33 words per 32 rows (cs_stage_codes: conflict-free row
+// reads, conflict-free writes, in place over the tile's first 8.25 KiB), and thread
+// u packs rows [32u, 32u + 32) = exactly W output words from 32 conflict-free
+// loads (bank (33u + i) mod 32), every shift a compile-time constant.
+constexpr uint32_t kCsNarrow = 16;  // widest block of the staged path
+constexpr uint32_t kCsUnitStride = 33;
+
+template <int W>
+__device__ __forceinline__ void cs_pack_unit(const uint32_t* __restrict__ c, uint32_t* __restrict__ dst) {
+  constexpr int V = (W % 4 == 0) ? 4 : ((W % 2 == 0) ? 2 : 1);
+  uint32_t o[V];
+  uint64_t acc = 0;
+  int filled = 0, k = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    acc |= (uint64_t)c[i] << filled;
+    filled += W;
+    if (filled >= 32) {
+      o[k % V] = (uint32_t)acc;
+      acc >>= 32;
+      filled -= 32;
+      ++k;
+      if (k % V == 0) {
+        if constexpr (V == 4) *reinterpret_cast<uint4*>(dst + k - 4) = make_uint4(o[0], o[1], o[2], o[3]);
+        else if constexpr (V == 2) *reinterpret_cast<uint2*>(dst + k - 2) = make_uint2(o[0], o[1]);
+        else dst[k - 1] = o[0];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cs_pack_unit_dispatch(uint32_t w, const uint32_t* c, uint32_t* dst) {
+  switch (w) {
+#define MS_CU_CASE(W) \
+  case W:             \
+    cs_pack_unit<W>(c, dst); \
+    break;
+    MS_CU_CASE(1) MS_CU_CASE(2) MS_CU_CASE(3) MS_CU_CASE(4) MS_CU_CASE(5) MS_CU_CASE(6) MS_CU_CASE(7)
+    MS_CU_CASE(8) MS_CU_CASE(9) MS_CU_CASE(10) MS_CU_CASE(11) MS_CU_CASE(12) MS_CU_CASE(13) MS_CU_CASE(14)
+    MS_CU_CASE(15) MS_CU_CASE(16)
+#undef MS_CU_CASE
     default:
       break;
   }
@@ -214,11 +266,40 @@ __global__ void __launch_bounds__(kCsThreads, 1)
         W.w[lane] = w;
         W.ex[lane] = incl - w;
       }
+      const uint32_t wm = __reduce_max_sync(kFull, w);
+      if (lane == 0) W.wmax = wm;
     }
     cs_bar(p);
     // pack: thread tt builds u32 words tt, tt + 64, ... of each block from the codes overlapping them,
     // at the block's width as a compile-time constant (cs_pack_block<W>)
     uint32_t* slot32 = reinterpret_cast<uint32_t*>(o.slots + t * kChunk);
+    if (nmain == (uint32_t)kChunk && W.wmax <= kCsNarrow) {
+      // narrow tile: stage the codes as u32 (their low words are exact: w <= 16), 33 words per
+      // 32 rows, over the tile itself. Batch tb = rows [512 tb, 512 tb + 512): read into
+      // registers, barrier, write words [528 tb, 528 tb + 528) = rows [264 tb, 264 tb + 264) of
+      // the tile, all read in this or an earlier batch; later batches read rows >= 512 tb + 511.
+      uint32_t* C = reinterpret_cast<uint32_t*>(V);
+#pragma unroll 1
+      for (uint32_t tb = 0; tb < kChunk / 512; ++tb) {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t i = (16 * tb + 2 * k + h) * 32 + lane;
+          const uint32_t v = (uint32_t)V[i];
+          if (is_delta) c[k] = (i & (B - 1)) ? v - (uint32_t)V[i - 1] : 0u;
+          else if (is_for) c[k] = v - (uint32_t)W.lo[i >> lg];
+          else c[k] = v;
+        }
+        cs_bar(p);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) C[(16 * tb + 2 * k + h) * kCsUnitStride + lane] = c[k];
+      }
+      cs_bar(p);
+      const uint32_t b = (tt * 32) >> lg, wb = W.w[b];
+      if (wb)
+        cs_pack_unit_dispatch(wb, C + tt * kCsUnitStride,
+                              slot32 + (W.ex[b] << (lg - 5)) + (tt - (b << (lg - 5))) * wb);
+    } else {
     for (uint32_t b = 0; b < nbc; ++b) {
       const uint32_t wb = W.w[b];
       if (!wb) continue;
@@ -227,6 +308,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       uint32_t* dst = slot32 + (W.ex[b] << (lg - 5));
       if (is_delta) cs_pack_dispatch<true>(wb, cb, sub, B, dst, tt);
       else cs_pack_dispatch<false>(wb, cb, sub, B, dst, tt);
+    }
     }
     // rows past the last full block: the uncompressed remainder
     for (uint32_t i = nmain + tt; i < cnt; i += 32 * kCsPair) o.rem[r0 + i - nbm] = V[i];
