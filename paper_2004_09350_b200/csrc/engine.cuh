@@ -293,24 +293,31 @@ __device__ __forceinline__ void encode_tile(const OutView& o, uint32_t item, uin
 }
 
 // slot mode, second half: tile k's packed blocks (slot words [0, (cwx[kb1] - cwx[kb0]) * B / 64))
-// -> payload word cwx[kb0] * B / 64, and cw[b + 1] = cwx[b + 1] for its blocks. One CTA per tile.
+// -> payload word cwx[kb0] * B / 64, and cw[b + 1] = cwx[b + 1] for its blocks. One warp per tile
+// (a CTA per tile left most threads idle on narrow tiles — 1.3 KB at 5 bits — and every tile
+// waits on its offsets before its copy: 8x the tiles in flight per SM).
 static __global__ void __launch_bounds__(256) tile_copy_kernel(OutView o, uint64_t n_tiles, uint64_t nb, const uint64_t* cwx,
                                                         uint32_t* err) {
   const uint32_t per = kChunk >> o.log2B;  // blocks per full tile
-  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  const uint32_t lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
+  const uint64_t n_warps = (uint64_t)gridDim.x * wpc;
+  for (uint64_t t = (uint64_t)blockIdx.x * wpc + (threadIdx.x >> 5); t < n_tiles; t += n_warps) {
     const uint64_t kb0 = t * per;
     if (kb0 >= nb) break;
     const uint64_t kb1 = min(kb0 + per, nb);
-    const uint64_t E = cwx[kb0];
-    const uint64_t words = (cwx[kb1] - E) * (o.B / 64);
-    for (uint64_t b = kb0 + threadIdx.x; b < kb1; b += blockDim.x) {
-      if (cwx[b + 1] > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
-      o.cw[b + 1] = (uint32_t)cwx[b + 1];
+    const uint64_t E = __ldg(cwx + kb0);
+    const uint64_t words = (__ldg(cwx + kb1) - E) * (o.B / 64);
+    for (uint64_t b = kb0 + lane; b < kb1; b += 32) {
+      const uint64_t c1 = __ldg(cwx + b + 1);
+      if (c1 > 0xffffffffull) atomicOr(err, err_bit(MS_E_INVALID));  // D-4 limit
+      o.cw[b + 1] = (uint32_t)c1;
     }
     const ulonglong2* src = reinterpret_cast<const ulonglong2*>(o.slots + t * kChunk);
-    uint64_t* dst = o.payload + E * (o.B / 64);
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(o.payload + E * (o.B / 64));
     // B >= 128: the tile's words start 16-byte aligned on both sides (B/64 * w words, B/64 even)
-    for (uint64_t m = threadIdx.x; m < words / 2; m += blockDim.x) reinterpret_cast<ulonglong2*>(dst)[m] = src[m];
+    const uint64_t n2 = words / 2;
+#pragma unroll 4
+    for (uint64_t m = lane; m < n2; m += 32) dst[m] = src[m];
   }
 }
 

@@ -268,8 +268,8 @@ cudaError_t launch_engine_gather(const ColView& pos, const ColView& data, uint64
 cudaError_t launch_tile_copy(const OutView& o, uint64_t n_tiles, uint64_t nb, const uint64_t* cwx, uint32_t* err,
                              cudaStream_t s) {
   if (!n_tiles || !nb) return cudaSuccess;
-  uint64_t g = n_tiles;
-  if (g > (uint64_t)num_sms() * 16) g = num_sms() * 16;
+  uint64_t g = (n_tiles + 7) / 8;  // a warp per tile, 8 warps per CTA
+  if (g > (uint64_t)num_sms() * 8) g = num_sms() * 8;
   ProfScope prof_("tile_copy", s);
   tile_copy_kernel<<<(int)g, 256, 0, s>>>(o, n_tiles, nb, cwx, err);
   return cudaGetLastError();
