@@ -5,8 +5,8 @@
 // __syncthreads and ~6,700 warp instructions per tile).
 //
 // compress_stream_kernel: persistent, one CTA per SM, each CTA a contiguous run of
-// tiles; warp 0 issues one TMA bulk copy per tile (16 KiB) into stage li % 12
-// (mbarrier complete_tx); consumer pair li % 12 (two warps, no CTA barrier):
+// tiles; warp 0 issues one TMA bulk copy per tile (16 KiB) into stage li % 13
+// (mbarrier complete_tx); consumer pair li % 13 (two warps, no CTA barrier):
 //   pass 1  per block, warp h takes the 32-row groups h, h + 2, ... (row 32g +
 //           lane): FOR: the extremes; DYN / DELTA: the OR of the values (DELTA: of
 //           d = v - v_prev, d_0 = 0, D-6) — ebw(max) = ebw(OR) — reduced across
@@ -26,7 +26,7 @@
 
 namespace ms {
 
-constexpr int kCsStages = 12;
+constexpr int kCsStages = 13;
 constexpr int kCsPair = 2;  // consumer warps per stage
 constexpr int kCsThreads = (1 + kCsPair * kCsStages) * 32;
 
@@ -46,7 +46,7 @@ __device__ __forceinline__ void cs_bar(uint32_t id) { asm volatile("bar.sync %0,
 // (B * W / 32 words): word m starts inside code j = 32m / W (a division by a
 // constant) at bit sh = 32m - jW; the codes j + 1, ... that fill it follow, at
 // most 32 / W + 1 of them (DELTA: code = v_j - v_{j-1}, code 0 = 0; else v - sub).
-template <int W, bool DELTA>
+template <int W, bool DELTA, bool SUB>
 __device__ __forceinline__ void cs_pack_block(const uint64_t* __restrict__ cb, uint64_t sub, uint32_t B,
                                               uint32_t* __restrict__ dst, uint32_t tt) {
   constexpr int K = 32 / W + 1;  // codes after the first that may overlap one word
@@ -54,7 +54,7 @@ __device__ __forceinline__ void cs_pack_block(const uint64_t* __restrict__ cb, u
   for (uint32_t m = tt; m < nw; m += 32 * kCsPair) {
     const uint32_t bit0 = m * 32, j = bit0 / (uint32_t)W, sh = bit0 - j * (uint32_t)W;
     uint64_t v = cb[j];
-    uint64_t prev = DELTA ? (j ? cb[j - 1] : v) : sub;  // DELTA: the previous value carried along
+    uint64_t prev = DELTA ? (j ? cb[j - 1] : v) : (SUB ? sub : 0ull);  // DELTA: the previous value carried along
     uint64_t acc = (v - prev) >> sh;
     uint32_t filled = (uint32_t)W - sh;
 #pragma unroll
@@ -70,13 +70,13 @@ __device__ __forceinline__ void cs_pack_block(const uint64_t* __restrict__ cb, u
   }
 }
 
-template <bool DELTA>
+template <bool DELTA, bool SUB>
 __device__ __forceinline__ void cs_pack_dispatch(uint32_t w, const uint64_t* cb, uint64_t sub, uint32_t B,
                                                  uint32_t* dst, uint32_t tt) {
   switch (w) {
 #define MS_CS_CASE(W) \
   case W:             \
-    cs_pack_block<W, DELTA>(cb, sub, B, dst, tt); \
+    cs_pack_block<W, DELTA, SUB>(cb, sub, B, dst, tt); \
     break;
     MS_CS_CASE(1) MS_CS_CASE(2) MS_CS_CASE(3) MS_CS_CASE(4) MS_CS_CASE(5) MS_CS_CASE(6) MS_CS_CASE(7)
     MS_CS_CASE(8) MS_CS_CASE(9) MS_CS_CASE(10) MS_CS_CASE(11) MS_CS_CASE(12) MS_CS_CASE(13) MS_CS_CASE(14)
@@ -306,8 +306,9 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       const uint64_t* cb = V + (b << lg);
       const uint64_t sub = is_for ? W.lo[b] : 0ull;
       uint32_t* dst = slot32 + (W.ex[b] << (lg - 5));
-      if (is_delta) cs_pack_dispatch<true>(wb, cb, sub, B, dst, tt);
-      else cs_pack_dispatch<false>(wb, cb, sub, B, dst, tt);
+      if (is_delta) cs_pack_dispatch<true, false>(wb, cb, sub, B, dst, tt);
+      else if (is_for) cs_pack_dispatch<false, true>(wb, cb, sub, B, dst, tt);
+      else cs_pack_dispatch<false, false>(wb, cb, sub, B, dst, tt);  // DYN: the values themselves
     }
     }
     // rows past the last full block: the uncompressed remainder
