@@ -796,6 +796,7 @@ __global__ void __launch_bounds__(kThreads) rle_write_kernel(const uint64_t* __r
       a[q] = r < n ? __ldg(v + r) : 0ull;
       b[q] = (r >= 1 && r < n) ? __ldg(v + r - 1) : ~a[q];
     }
+    const uint64_t off = __ldg(chunk_off + t);  // with the rows: not a second dependent load after the scan
     uint32_t bal[kVPT];
 #pragma unroll
     for (int q = 0; q < kVPT; ++q) {
@@ -817,7 +818,6 @@ __global__ void __launch_bounds__(kThreads) rle_write_kernel(const uint64_t* __r
       grp[2 * tid + 1] = ex + c0;
     }
     __syncthreads();
-    const uint64_t off = chunk_off[t];
     const uint32_t below = (1u << lane) - 1u;
 #pragma unroll
     for (int q = 0; q < kVPT; ++q)
