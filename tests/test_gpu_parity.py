@@ -374,7 +374,7 @@ def test_select_stream_many_chunks(fname, rng):
 @pytest.mark.parametrize("kind", ["small", "sorted", "wide"])
 def test_compress_stream_stage_reuse(kind, rng):
     """u64 -> DYN / FOR / DELTA_BP through the streamed compress (cstream.cuh) with
-    more 2048-row tiles per CTA than its 10 stages, every block size, a ragged
+    more 2048-row tiles per CTA than its 13 stages, every block size, a ragged
     tail; byte-exact against the oracle."""
     ms = get_ms()
     n = (1 << 23) + 77
@@ -385,6 +385,37 @@ def test_compress_stream_stage_reuse(kind, rng):
     try:
         for f in (ms.dyn_bp(128), ms.for_bp(512), ms.delta_bp(2048), ms.delta_bp(256), ms.for_bp(1024)):
             assert_same_image(ms.compress(t, f), O.encode(v, *oracle_fmt(f)), f"compress {f} {kind}")
+        names = set(ms.profile_read())
+    finally:
+        ms.profile_enable(False)
+    assert "compress_stream" in names
+
+
+@pytest.mark.parametrize("kind", ["values", "steps"])
+def test_compress_stream_narrow_and_wide_tiles(kind, rng):
+    """cstream.cuh picks its packer per 2048-row tile: the staged u32 packer when every
+    block of the tile is <= 16 bits wide, the word builder otherwise. Narrow values (or
+    steps) with rare 40-bit outliers mix both kinds of tile, and widths that differ
+    between the blocks of one tile, in one column; bases near a multiple of 2^32 make
+    the staged packer's low-word differences wrap. Byte-exact against the oracle."""
+    ms = get_ms()
+    n = (1 << 22) + 5
+    x = rng.integers(0, 1 << 10, n).astype(np.uint64)
+    x[(np.arange(n) >> 7) % 3 == 0] &= np.uint64(3)  # every third 128-row stretch narrower: widths differ inside a tile
+    hit = rng.random(n) < 1e-4                  # ~0.2 outliers per 2048-row tile
+    x[hit] = (np.uint64(1) << np.uint64(40)) + x[hit]
+    if kind == "values":
+        v = x + np.uint64((1 << 32) - 300)       # FOR: min just below 2^32, values across it
+    else:
+        v = np.cumsum(x, dtype=np.uint64) + np.uint64((1 << 32) - 5000)  # DELTA: narrow steps, rare wide ones
+    t = to_torch(v)
+    ms.profile_read()
+    ms.profile_enable(True)
+    try:
+        for f in (ms.dyn_bp(128), ms.for_bp(128), ms.for_bp(512), ms.delta_bp(256), ms.delta_bp(2048)):
+            g = ms.compress(t, f)
+            assert_same_image(g, O.encode(v, *oracle_fmt(f)), f"compress {f} {kind}")
+            assert np.array_equal(ms.to_u64_numpy(ms.decompress(g)), v)
         names = set(ms.profile_read())
     finally:
         ms.profile_enable(False)
